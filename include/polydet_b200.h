@@ -1,0 +1,106 @@
+/*
+ * polydet_b200 — C ABI of the B200 modular-determinant hot path.
+ *
+ * The reference (arXiv 2010.12117, package `polydet`) has no native code and
+ * no FFI: its hot path is four numpy functions called from the Python
+ * executor.  Each entry point below replaces one of them; the Python package
+ * `paper_2010_12117_b200` binds this library with ctypes and keeps the
+ * reference's Python signatures on top:
+ *
+ *   pdb_ntt_multi_u32        <- transform.py:119-159  ntt_forward_multi / ntt_inverse_multi
+ *   pdb_reduce_scatter_u32   <- tensor.py:214-237     reduce_mod + pad_to (per entry, per prime)
+ *   pdb_det_batch_u32        <- determinant.py:92-133 det_grid (with entry_ids indirection)
+ *   pdb_eval_det_fused_u32   <- pipeline.py:349-392   _fft_stage's last axis fused into _det_stage
+ *   pdb_crt_mrc_u32          <- crt.py:94-130         combine_tensor (digits + Horner + signed lift)
+ *   pdb_prime_ctx_*          <- transform.py:19-72    TwiddleTable (per-prime root tables)
+ *
+ * Conventions
+ *  - Every pointer argument named data/grids/partial/out/residues/limbs/neg/
+ *    scratch/mag/pos/entry_ids is a DEVICE pointer owned by the caller; the
+ *    library allocates nothing in hot calls (only pdb_prime_ctx_* allocate
+ *    their twiddle tables).  `primes` in pdb_crt_mrc_u32 is a HOST array.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream); calls are
+ *    stream-ordered and do not synchronise unless stated.
+ *  - Return 0 on success, <0 on error; pdb_last_error() gives a thread-local
+ *    message.  -2 = invalid argument (maps to ValueError), -1 = CUDA error.
+ *  - Residues are u32 in [0, p); this library handles primes p < 2^31
+ *    (the reference's default planning range, prime_start = 10^9).
+ */
+#ifndef POLYDET_B200_H
+#define POLYDET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pdb_prime_ctx pdb_prime_ctx;
+
+const char* pdb_last_error(void);
+int32_t pdb_version(void);
+int32_t pdb_device_sm_count(int32_t device);
+
+/* Prime p = c * 2^q + 1 with omega of exact order 2^q (reference PrimeSpec,
+ * modular.py:81-108).  Builds the Shoup/Montgomery constants. */
+int32_t pdb_prime_ctx_create(uint64_t p, uint64_t omega, int32_t q, pdb_prime_ctx** out);
+int32_t pdb_prime_ctx_destroy(pdb_prime_ctx* ctx);
+/* Build (synchronously) the device twiddle tables for transform length n. */
+int32_t pdb_prime_ctx_prepare(pdb_prime_ctx* ctx, int64_t n);
+
+/* In-place natural-order NTT of `batch` row-major tensors of shape dims[0..ndim)
+ * along every axis whose bit is set in axis_mask (inverse: w^-1 and * N^-1
+ * per axis with N > 1).  extents (may be NULL) = per axis, how many leading
+ * indices can be nonzero before that axis is transformed: lines outside the
+ * box are skipped (they are zero and stay zero).  Axes are processed from the
+ * last to the first.  Errors: length not a power of two or above 2^q
+ * ("unsupported length"). */
+int32_t pdb_ntt_multi_u32(pdb_prime_ctx* ctx, uint32_t* data, int64_t batch, int32_t ndim,
+                          const int64_t* dims, const int64_t* extents, uint32_t axis_mask,
+                          int32_t inverse, void* stream);
+
+/* dst[pos[i]] = (sign_i * sum_l mag[i*limbs + l] 2^(32 l)) mod p. */
+int32_t pdb_reduce_scatter_u32(pdb_prime_ctx* ctx, const uint32_t* mag, const uint8_t* neg,
+                               const int64_t* pos, int64_t count, int32_t limbs, uint32_t* dst,
+                               void* stream);
+
+/* det mod p of M(node) for node in [node_lo, node_lo + nodes), where
+ * M(node)[i][j] = grids[entry_ids[i*r + j] * grid_stride + node]; out[node - node_lo]. */
+size_t pdb_det_scratch_bytes(int32_t r, int64_t nodes);
+int32_t pdb_det_batch_u32(pdb_prime_ctx* ctx, const uint32_t* grids, int64_t grid_stride,
+                          const int32_t* entry_ids, int32_t r, int64_t node_lo, int64_t nodes,
+                          uint32_t* out, void* scratch, size_t scratch_bytes, void* stream);
+
+/* Same, with the entries evaluated on the fly: partial[(e*outer + o)*ncoef + l]
+ * holds entry e transformed along every axis but the last, l-th coefficient of
+ * the last variable; node = o * n_last + c is evaluated at w_{n_last}^c. */
+int32_t pdb_eval_det_fused_u32(pdb_prime_ctx* ctx, const uint32_t* partial, int64_t outer,
+                               int32_t ncoef, int32_t n_last, const int32_t* entry_ids, int32_t r,
+                               int64_t node_lo, int64_t nodes, uint32_t* out, void* scratch,
+                               size_t scratch_bytes, void* stream);
+
+/* Scalar condensation with the reference's pivot trail (determinant.py:57-84):
+ * mat = r*r row-major residues (device); trail_vals[i]/trail_cols[i] = pivot of
+ * step i (cols = -1 after an all-zero row); det_out[0] = det.  Scratch needs
+ * 4 r^2 + 256 + 512 r^2 bytes. */
+int32_t pdb_condense_u32(pdb_prime_ctx* ctx, const uint32_t* mat, int32_t r, uint32_t* trail_vals,
+                         int32_t* trail_cols, uint32_t* det_out, void* scratch, size_t scratch_bytes,
+                         void* stream);
+
+/* Mixed-radix CRT over nprimes residue rows residues[i*stride + pos], pos < n.
+ * limbs[pos*L + l] = |X| little-endian, neg[pos] = X < 0, X in (-P/2, P/2]. */
+int32_t pdb_crt_limbs(int32_t nprimes);
+size_t pdb_crt_scratch_bytes(int32_t nprimes);
+int32_t pdb_crt_mrc_u32(const uint32_t* residues, int32_t nprimes, int64_t n, int64_t stride,
+                        const uint32_t* primes, uint32_t* limbs, int32_t L, uint8_t* neg,
+                        void* scratch, size_t scratch_bytes, void* stream);
+
+/* Integer-pipe peak of an update primitive (no memory traffic), in updates/s.
+ * variant 0 = Shoup mul-mod + sub-mod, 1 = delayed 64-bit MAC (8 per REDC). */
+int32_t pdb_mulmod_peak(uint32_t p, int32_t variant, double* updates_per_second, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLYDET_B200_H */

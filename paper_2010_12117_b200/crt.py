@@ -1,0 +1,136 @@
+"""Chinese remaindering -- drop-in for the reference's `crt.py` (lines 20-130).
+
+`combine_tensor` runs the whole mixed-radix lift on the GPU
+(`pdb_crt_mrc_u32`: digits, multi-limb Horner and the signed lift) and the
+host only turns the returned limbs into Python ints.  `build_basis`,
+`horner_lift` and `signed_lift` are exact big-integer host helpers of the
+scalar API; `mrc_digits` reads the digits off the device-lifted value.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .fields import inv_mod
+from .layout import CoeffTensor
+
+
+@dataclass(frozen=True)
+class CrtBasis:
+    """weights[j] = p_0...p_{j-1}; inverses[i] = weights[i]^-1 mod p_i;
+    weight_residues[i][j] = weights[j] mod p_i; product = P."""
+
+    primes: tuple
+    weights: tuple
+    inverses: tuple
+    weight_residues: tuple
+    product: int
+
+
+def build_basis(primes) -> CrtBasis:
+    primes = tuple(int(p) for p in primes)
+    if not primes:
+        raise ValueError("at least one prime is required")
+    if len(set(primes)) < len(primes):
+        raise ValueError("duplicate primes in %s" % (primes,))
+    weights = [1]
+    for p in primes[:-1]:
+        weights.append(weights[-1] * p)
+    inverses = [1] + [inv_mod(weights[i] % primes[i], primes[i]) for i in range(1, len(primes))]
+    table = [()] + [tuple(w % primes[i] for w in weights[:i]) for i in range(1, len(primes))]
+    return CrtBasis(primes, tuple(weights), tuple(inverses), tuple(table), weights[-1] * primes[-1])
+
+
+def horner_lift(digits, basis: CrtBasis) -> int:
+    """sum_j digits[j] * weights[j], folded from the top digit."""
+    if len(digits) != len(basis.primes):
+        raise ValueError("got %d digits for %d primes" % (len(digits), len(basis.primes)))
+    value = int(digits[-1])
+    for d, p in zip(reversed(digits[:-1]), reversed(basis.primes[:-1])):
+        value = value * p + int(d)
+    return value
+
+
+def signed_lift(x: int, product: int) -> int:
+    """[0, P) -> (-P/2, P/2]."""
+    if not 0 <= x < product:
+        raise ValueError("%d is not a canonical residue mod %d" % (x, product))
+    return x - product if 2 * x > product else x
+
+
+def limbs_to_ints(limbs: np.ndarray, neg: np.ndarray) -> list:
+    """Device CRT output (|X| as LE u32 limbs + sign) -> Python ints."""
+    n, L = limbs.shape
+    out = [0] * n
+    nonzero = np.flatnonzero(limbs.any(axis=1))
+    if nonzero.size == 0:
+        return out
+    small = limbs[nonzero, 2:].any(axis=1) == 0 if L > 2 else np.ones(nonzero.size, dtype=bool)
+    sidx = nonzero[small]
+    if sidx.size:
+        mag = limbs[sidx, 0].astype(np.int64) | (limbs[sidx, 1].astype(np.int64) << 32) if L > 1 \
+            else limbs[sidx, 0].astype(np.int64)
+        big2 = (limbs[sidx, 1] >> 31).astype(bool) if L > 1 else np.zeros(sidx.size, dtype=bool)
+        vals = np.where(neg[sidx].astype(bool), -mag, mag)
+        for i, v, b in zip(sidx.tolist(), vals.tolist(), big2.tolist()):
+            out[i] = v
+        # magnitudes >= 2^63 do not fit int64: redo those exactly
+        for i in sidx[big2].tolist():
+            v = int.from_bytes(limbs[i].tobytes(), "little")
+            out[i] = -v if neg[i] else v
+    bidx = nonzero[~small]
+    if bidx.size:
+        rows = limbs[bidx]
+        raw = rows.tobytes()
+        width = 4 * L
+        negs = neg[bidx].tolist()
+        for j, i in enumerate(bidx.tolist()):
+            v = int.from_bytes(raw[j * width:(j + 1) * width], "little")
+            out[i] = -v if negs[j] else v
+    return out
+
+
+def device_lift(residues_dev, primes, n: int, stride: int) -> list:
+    """CRT of device residue rows [P][stride] -> list of n Python ints."""
+    torch = native._torch()
+    P = len(primes)
+    L = native.crt_limbs(P)
+    dev = residues_dev.device
+    limbs = torch.empty((n, L), dtype=torch.int32, device=dev)
+    neg = torch.empty(n, dtype=torch.uint8, device=dev)
+    scratch = native.scratch_tensor(native.crt_scratch_bytes(P), dev)
+    native.crt_mrc(residues_dev, P, n, stride, primes, limbs, L, neg, scratch)
+    return limbs_to_ints(native.to_host_u32(limbs).reshape(n, L), neg.cpu().numpy())
+
+
+def mrc_digits(residues, basis: CrtBasis) -> list:
+    """Mixed-radix digits: X = sum digits[j] weights[j], 0 <= digits[j] < p_j."""
+    if len(residues) != len(basis.primes):
+        raise ValueError("got %d residues for %d primes" % (len(residues), len(basis.primes)))
+    vals = np.array([[int(x) % p] for x, p in zip(residues, basis.primes)], dtype=np.int64)
+    value = device_lift(native.to_device_u32(vals), basis.primes, 1, 1)[0]
+    if value < 0:
+        value += basis.product
+    digits = []
+    for p in basis.primes:
+        value, d = divmod(value, p)
+        digits.append(d)
+    return digits
+
+
+def combine_tensor(residue_tensors) -> CoeffTensor:
+    """Exact signed coefficients from one residue tensor per prime."""
+    if not residue_tensors:
+        raise ValueError("at least one residue tensor is required")
+    shape = residue_tensors[0].shape
+    names = residue_tensors[0].axis_vars
+    if any(t.shape != shape or t.axis_vars != names for t in residue_tensors):
+        raise ValueError("residue tensors must share one shape")
+    basis = build_basis([t.prime.p for t in residue_tensors])
+    n = residue_tensors[0].size
+    stacked = np.stack([np.asarray(t.residues, dtype=object).astype(np.int64) for t in residue_tensors])
+    coeffs = device_lift(native.to_device_u32(stacked), basis.primes, n, n)
+    return CoeffTensor(tuple(shape), tuple(coeffs), tuple(names))

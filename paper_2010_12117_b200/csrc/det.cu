@@ -1,0 +1,219 @@
+// Determinants mod p of the r x r matrices at every evaluation node.
+//
+// The value is algorithm independent (reference determinant.py:1-8), so the
+// kernels are free to choose their elimination order; they all return the
+// exact det(M) mod p in [0, p).  Three kernels:
+//
+//  * det_small<R>   R <= 8: one lane per matrix, the matrix in registers,
+//                   division-free elimination with diagonal pivots.
+//  * det_octet      9 <= r <= 64 and p < 2^30: eight lanes per matrix, the
+//                   matrix in shared memory, blocked division-free elimination
+//                   with delayed (64-bit accumulate + Montgomery) reduction
+//                   (det_octet.cuh).
+//  * det_robust     any r <= 64, any p < 2^31: one thread per matrix with the
+//                   reference's exact pivot rule (first nonzero column of row
+//                   i, determinant.py:136-169) and full division-free updates.
+//
+// The fast kernels only take diagonal pivots; a matrix whose diagonal pivot
+// vanishes is appended to a node list and recomputed by det_robust, so every
+// input (singular, structured, permuted) gets the exact answer.
+#include <vector>
+#include "pdb_internal.cuh"
+#include "det_octet.cuh"
+
+namespace pdb {
+
+struct FlagList {
+  unsigned long long* count;
+  int64_t* nodes;
+};
+
+__device__ __forceinline__ void flag_node(FlagList f, int64_t node) {
+  unsigned long long slot = atomicAdd(f.count, 1ull);
+  f.nodes[slot] = node;
+}
+
+// ---------------------------------------------------------------- robust ----
+template <class Src>
+__global__ void __launch_bounds__(128)
+det_robust(Src src, const int32_t* __restrict__ ids, int r, const int64_t* __restrict__ list,
+           const unsigned long long* __restrict__ list_count, int64_t count, int64_t node_lo,
+           uint32_t* __restrict__ out, uint32_t* __restrict__ scratch, Mod32 m,
+           uint32_t* __restrict__ trail_vals = nullptr, int32_t* __restrict__ trail_cols = nullptr) {
+  const int64_t slots = (int64_t)gridDim.x * blockDim.x;
+  const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t total = list ? (int64_t)*list_count : count;
+  const uint32_t p = m.p;
+  uint32_t* A = scratch + slot;
+  auto at = [&](int i, int j) -> uint32_t& { return A[(int64_t)(i * r + j) * slots]; };
+  for (int64_t idx = slot; idx < total; idx += slots) {
+    const int64_t node = list ? list[idx] : node_lo + idx;
+    for (int e = 0; e < r * r; ++e) at(e / r, e % r) = src.get(ids[e], node);
+    uint32_t pre = 1 % p, infl = 1 % p;
+    uint64_t used = 0;
+    int parity = 0;
+    bool alive = true;
+    for (int i = 0; i < r && alive; ++i) {
+      int c = -1;
+      for (int j = 0; j < r; ++j)
+        if (at(i, j)) { c = j; break; }
+      if (c < 0) { alive = false; break; }
+      const uint32_t z = at(i, c);
+      if (trail_vals) { trail_vals[i] = z; trail_cols[i] = c; }
+      parity ^= __popcll(used >> c) & 1;   // earlier pivot columns to the right of c
+      used |= 1ull << c;
+      pre = mul_mod(pre, z, m);
+      if (i + 1 < r) infl = mul_mod(infl, pre, m);
+      for (int k = i + 1; k < r; ++k) {
+        const uint32_t t = at(k, c);
+        for (int j = 0; j < r; ++j)
+          at(k, j) = sub_mod(mul_mod(z, at(k, j), m), mul_mod(t, at(i, j), m), p);
+      }
+    }
+    uint32_t det = 0;
+    if (alive) {
+      det = mul_mod(pre, inv_mod(infl, m), m);
+      if (parity && det) det = p - det;
+    }
+    out[node - node_lo] = det;
+  }
+}
+
+// ----------------------------------------------------------------- small ----
+template <int R, class Src>
+__global__ void __launch_bounds__(128)
+det_small(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t nodes,
+          uint32_t* __restrict__ out, FlagList flags, Mod32 m) {
+  __shared__ int32_t ids[R * R];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) ids[e] = ids_g[e];
+  __syncthreads();
+  const uint32_t p = m.p;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < nodes;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t node = node_lo + idx;
+    uint32_t a[R][R];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int j = 0; j < R; ++j) a[i][j] = src.get(ids[i * R + j], node);
+    uint32_t pre = 1 % p, infl = 1 % p;
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const uint32_t z = a[k][k];
+      ok = ok && z != 0;
+      pre = mul_mod(pre, z, m);
+      if (k + 1 < R) infl = mul_mod(infl, pre, m);
+      const uint32_t zs = shoup_companion_fast(z, m);
+#pragma unroll
+      for (int i = k + 1; i < R; ++i) {
+        const uint32_t t = a[i][k];
+        const uint32_t ts = shoup_companion_fast(t, m);
+#pragma unroll
+        for (int j = k + 1; j < R; ++j)
+          a[i][j] = sub_mod(shoup_mul(a[i][j], z, zs, p), shoup_mul(a[k][j], t, ts, p), p);
+      }
+    }
+    if (ok) {
+      out[idx] = mul_mod(pre, inv_mod(infl, m), m);
+    } else {
+      flag_node(flags, node);
+    }
+  }
+}
+
+template <class Src>
+static int launch_small(int r, Src src, const int32_t* ids, int64_t lo, int64_t n, uint32_t* out,
+                        FlagList f, Mod32 m, int grid, cudaStream_t st) {
+  switch (r) {
+#define PDB_SMALL(R) case R: det_small<R, Src><<<grid, 128, 0, st>>>(src, ids, lo, n, out, f, m); break;
+    PDB_SMALL(1) PDB_SMALL(2) PDB_SMALL(3) PDB_SMALL(4)
+    PDB_SMALL(5) PDB_SMALL(6) PDB_SMALL(7) PDB_SMALL(8)
+#undef PDB_SMALL
+    default: return -1;
+  }
+  return 0;
+}
+
+int robust_slots(int r) {
+  // bounded scratch for the fallback: at most 16 Mi words of matrices
+  int64_t t = (16ll << 20) / ((int64_t)r * r);
+  if (t > 65536) t = 65536;
+  if (t < 128) t = 128;
+  return (int)(t / 128 * 128);
+}
+
+size_t det_scratch_bytes(int r, int64_t nodes) {
+  const size_t robust_threads = robust_slots(r);
+  return 256 + sizeof(int64_t) * (size_t)nodes + sizeof(uint32_t) * (size_t)r * r * robust_threads;
+}
+
+template <class Src>
+int det_run(PrimeCtx* ctx, Src src, const int32_t* ids, int r, int64_t node_lo, int64_t nodes,
+            uint32_t* out, void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  if (r < 1 || r > PDB_MAX_ORDER) {
+    set_error("unsupported matrix order %d (1..%d)", r, PDB_MAX_ORDER);
+    return -2;
+  }
+  if (nodes == 0) return 0;
+  if (scratch_bytes < det_scratch_bytes(r, nodes)) {
+    set_error("det scratch too small: %zu < %zu", scratch_bytes, det_scratch_bytes(r, nodes));
+    return -2;
+  }
+  char* base = static_cast<char*>(scratch);
+  FlagList flags{reinterpret_cast<unsigned long long*>(base), reinterpret_cast<int64_t*>(base + 256)};
+  uint32_t* mats = reinterpret_cast<uint32_t*>(base + 256 + sizeof(int64_t) * (size_t)nodes);
+  const Mod32 m = ctx->m;
+  const int slots = robust_slots(r);
+  bool fast = false;
+  if (cudaMemsetAsync(flags.count, 0, sizeof(unsigned long long), st) != cudaSuccess)
+    return check_launch("det memset");
+  if (r <= 8) {
+    int64_t blocks = (nodes + 127) / 128;
+    int grid = (int)(blocks < (int64_t)ctx->sms * 32 ? blocks : (int64_t)ctx->sms * 32);
+    launch_small(r, src, ids, node_lo, nodes, out, flags, m, grid, st);
+    fast = true;
+  } else if (m.fast()) {
+    if (launch_octet(ctx, r, src, ids, node_lo, nodes, out, flags.count, flags.nodes, st) == 0) fast = true;
+  }
+  if (int rc = check_launch("det fast path")) return rc;
+  if (fast) {
+    det_robust<Src><<<slots / 128, 128, 0, st>>>(src, ids, r, flags.nodes, flags.count, 0, node_lo,
+                                                  out, mats, m);
+  } else {
+    det_robust<Src><<<slots / 128, 128, 0, st>>>(src, ids, r, nullptr, nullptr, nodes, node_lo,
+                                                  out, mats, m);
+  }
+  return check_launch("det_robust");
+}
+
+int condense_run(PrimeCtx* ctx, const uint32_t* mat, int r, uint32_t* trail_vals, int32_t* trail_cols,
+                 uint32_t* det_out, void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  if (r < 1 || r > PDB_MAX_ORDER) {
+    set_error("unsupported matrix order %d (1..%d)", r, PDB_MAX_ORDER);
+    return -2;
+  }
+  const size_t need = sizeof(int32_t) * r * r + 256 + sizeof(uint32_t) * (size_t)r * r * 128;
+  if (scratch_bytes < need) {
+    set_error("condense scratch too small");
+    return -2;
+  }
+  std::vector<int32_t> ids(r * r);
+  for (int e = 0; e < r * r; ++e) ids[e] = e;
+  int32_t* d_ids = static_cast<int32_t*>(scratch);
+  uint32_t* mats = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) + ((sizeof(int32_t) * r * r + 255) & ~size_t(255)));
+  cudaMemcpyAsync(d_ids, ids.data(), sizeof(int32_t) * r * r, cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(trail_cols, 0xff, sizeof(int32_t) * r, st);
+  cudaStreamSynchronize(st);
+  StagedSrc src{mat, 1};
+  det_robust<StagedSrc><<<1, 128, 0, st>>>(src, d_ids, r, nullptr, nullptr, 1, 0, det_out, mats, ctx->m,
+                                           trail_vals, trail_cols);
+  return check_launch("condense");
+}
+
+template int det_run<StagedSrc>(PrimeCtx*, StagedSrc, const int32_t*, int, int64_t, int64_t,
+                                uint32_t*, void*, size_t, cudaStream_t);
+template int det_run<FusedSrc>(PrimeCtx*, FusedSrc, const int32_t*, int, int64_t, int64_t,
+                               uint32_t*, void*, size_t, cudaStream_t);
+
+}  // namespace pdb

@@ -1,0 +1,127 @@
+// Word-size modular arithmetic for the sm_100a kernels.
+//
+// All moduli on the 32-bit path satisfy p < 2^31 (so 2p < 2^32); the fast
+// elimination kernels additionally require p < 2^30 (see Mod32::fast()).
+//
+// Primitives (cost in fma-heavy issue slots, measured on B200: IMAD = 1,
+// IMAD.HI = IMAD.WIDE = 2; see profiles/intpipe_r01.json):
+//   shoup_mul(x, w, w')  x*w mod p in [0, 2p) for a constant w          (2 IMAD + 1 IMAD.HI)
+//   mul(a, b)            a*b mod p for two variables (Barrett, 64-bit)  (~6 IMAD-class)
+//   redc(acc)            acc * 2^-32 mod p in [0, 2^32) for acc < (2^32-p-1) 2^32
+//   canon32(v)           v mod p for any 32-bit v                       (IMAD.HI + IMAD + 1 ALU)
+#pragma once
+#include <cstdint>
+
+#define PDB_HD __host__ __device__ __forceinline__
+
+struct Mod32 {
+  uint32_t p;        // the prime
+  uint32_t pinv;     // -p^-1 mod 2^32 (Montgomery)
+  uint32_t mu;       // floor(2^32 / p)   (canon32)
+  uint32_t r2;       // 2^64 mod p        (to_mont)
+  uint32_t r1;       // 2^32 mod p
+  uint32_t r1s;      // Shoup companion of r1
+  uint64_t m64;      // floor(2^64 / p)   (Barrett for 64-bit products)
+
+  PDB_HD bool fast() const { return p < (1u << 30); }
+};
+
+PDB_HD uint32_t umulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(a, b);
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+
+PDB_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+// min(x, x - m) as unsigned: subtracts m once if x >= m (x < 2m).
+PDB_HD uint32_t csub(uint32_t x, uint32_t m) {
+  uint32_t y = x - m;
+  return y < x ? y : x;
+}
+
+PDB_HD uint32_t add_mod(uint32_t a, uint32_t b, uint32_t p) { return csub(a + b, p); }
+PDB_HD uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) { return csub(a + p - b, p); }
+
+// Shoup companion floor(w * 2^32 / p) for w < p (host or device; slow path).
+PDB_HD uint32_t shoup_companion(uint32_t w, uint32_t p) {
+  return (uint32_t)(((uint64_t)w << 32) / p);
+}
+
+// Shoup companion via the precomputed floor(2^64/p): q = floor(w*2^32/p) exactly.
+// q_est = floor(w * m64 / 2^32) = w*m_hi + hi(w*m_lo) is the exact quotient or
+// one below it; the remainder w*2^32 - q*p < 2p fits 32 bits, so it is
+// computed mod 2^32 as -q*p.
+PDB_HD uint32_t shoup_companion_fast(uint32_t w, const Mod32& m) {
+  uint32_t q = w * (uint32_t)(m.m64 >> 32) + umulhi32(w, (uint32_t)m.m64);
+  uint32_t r = 0u - q * m.p;
+  return r >= m.p ? q + 1 : q;
+}
+
+// x*w mod p, result in [0, 2p). Valid for any 32-bit x, w < p, ws = companion.
+PDB_HD uint32_t shoup_lazy(uint32_t x, uint32_t w, uint32_t ws, uint32_t p) {
+  uint32_t q = umulhi32(x, ws);
+  return x * w - q * p;
+}
+
+PDB_HD uint32_t shoup_mul(uint32_t x, uint32_t w, uint32_t ws, uint32_t p) {
+  return csub(shoup_lazy(x, w, ws, p), p);
+}
+
+// a*b mod p for variables a, b < 2^31 (p < 2^31): Barrett on the 62-bit product.
+PDB_HD uint32_t mul_mod(uint32_t a, uint32_t b, const Mod32& m) {
+  uint64_t t = (uint64_t)a * b;
+  uint64_t q = umulhi64(t, m.m64);
+  uint64_t r = t - q * m.p;          // in [0, 2p)
+  return csub((uint32_t)r, m.p);
+}
+
+// Montgomery reduction: returns v == acc * 2^-32 (mod p) with v < 2^32,
+// valid whenever acc < (2^32 - p - 1) * 2^32 (e.g. <= 12 products of residues
+// when p < 2^30).
+PDB_HD uint32_t redc(uint64_t acc, const Mod32& m) {
+  uint32_t mq = (uint32_t)acc * m.pinv;
+  uint64_t s = (uint64_t)mq * m.p + acc;  // exact: no 64-bit overflow under the bound
+  return (uint32_t)(s >> 32);
+}
+
+// Any 32-bit v -> [0, p).
+PDB_HD uint32_t canon32(uint32_t v, const Mod32& m) {
+  uint32_t q = umulhi32(v, m.mu);
+  return csub(v - q * m.p, m.p);
+}
+
+PDB_HD uint32_t pow_mod(uint32_t a, uint64_t e, const Mod32& m) {
+  uint32_t r = 1 % m.p, b = a;
+  while (e) {
+    if (e & 1) r = mul_mod(r, b, m);
+    b = mul_mod(b, b, m);
+    e >>= 1;
+  }
+  return r;
+}
+
+PDB_HD uint32_t inv_mod(uint32_t a, const Mod32& m) { return pow_mod(a, m.p - 2, m); }
+
+// Host-side construction of the constants.
+inline Mod32 make_mod32(uint32_t p) {
+  Mod32 m;
+  m.p = p;
+  uint32_t inv = 1;  // Newton iteration for p^-1 mod 2^32
+  for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
+  m.pinv = 0u - inv;
+  m.mu = (uint32_t)((((uint64_t)1) << 32) / p);
+  m.r1 = (uint32_t)((((uint64_t)1) << 32) % p);
+  m.r2 = (uint32_t)(((unsigned __int128)1 << 64) % p);
+  m.r1s = shoup_companion(m.r1, p);
+  m.m64 = (uint64_t)(((unsigned __int128)1 << 64) / p);
+  return m;
+}

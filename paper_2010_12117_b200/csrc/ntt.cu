@@ -1,0 +1,205 @@
+// Batched multivariate number-theoretic transforms (natural order in and out).
+//
+// Semantics follow the reference's `_multi` (transform.py:119-143): every
+// axis of a row-major tensor gets the length-N_a transform
+//     out[k] = sum_j x[j] * w^(jk),  w = omega^(2^(q - log2 N_a))
+// (inverse: w^-1 and a final * N_a^-1 when N_a > 1).  The reference rotates
+// the tensor after each axis pass; here every axis is transformed in place
+// through its stride, so no transposition pass exists at all.
+//
+// Kernel: one CTA owns a tile of LO lines x TI neighbouring inner indices
+// (TI consecutive words per row -> coalesced loads even for strided axes),
+// loads it into shared memory in bit-reversed row order and runs the log2 N
+// radix-2 DIT stages there with Shoup twiddles.  Lines that are entirely
+// zero (outside the coefficient box on not-yet-transformed axes) are skipped
+// ("pruning"): for an entry with (d+1)^vn coefficients only the first pass
+// touches (d+1)^(vn-1) lines per entry.
+#include "pdb_internal.cuh"
+
+namespace pdb {
+
+struct AxisGeom {
+  int64_t inner;           // product of dims after the axis
+  int32_t nbox;            // number of box dims describing active outer lines
+  int64_t box_ext[PDB_MAX_DIMS + 1];   // active extent per outer dim (slowest first)
+  int64_t box_dim[PDB_MAX_DIMS + 1];   // full dim per outer dim
+  int64_t active_outer;    // product of box_ext
+};
+
+__device__ __forceinline__ int64_t outer_offset(int64_t c, const AxisGeom& g) {
+  // compact active index -> real outer line index (mixed radix)
+  int64_t off = 0, mul = 1;
+  for (int d = g.nbox - 1; d >= 0; --d) {
+    int64_t e = g.box_ext[d];
+    int64_t i = c % e;
+    c /= e;
+    off += i * mul;
+    mul *= g.box_dim[d];
+  }
+  return off;
+}
+
+__device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) {
+  return bits ? (__brev(x) >> (32 - bits)) : 0u;
+}
+
+template <bool INV>
+__global__ void __launch_bounds__(256)
+ntt_axis_smem(uint32_t* __restrict__ data, AxisGeom g, int N, int logN, int TI, int LO,
+              const uint32_t* __restrict__ tw, const uint32_t* __restrict__ tws,
+              uint32_t ninv, uint32_t ninvs, Mod32 m) {
+  extern __shared__ uint32_t sm[];
+  const int64_t tchunks = (g.inner + TI - 1) / TI;
+  const int64_t ntiles = ((g.active_outer + LO - 1) / LO) * tchunks;
+  const int tile_words = LO * N * TI;
+  const uint32_t p = m.p;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t oc0 = (tile / tchunks) * LO;
+    const int64_t t0 = (tile % tchunks) * TI;
+    // load (bit-reversed rows)
+    for (int w = threadIdx.x; w < tile_words; w += blockDim.x) {
+      int t = w % TI;
+      int n = (w / TI) % N;
+      int lo = w / (TI * N);
+      int64_t oc = oc0 + lo;
+      uint32_t v = 0;
+      if (oc < g.active_outer && t0 + t < g.inner) {
+        int64_t base = outer_offset(oc, g) * (int64_t)N * g.inner;
+        v = data[base + (int64_t)n * g.inner + t0 + t];
+      }
+      sm[(lo * N + bitrev(n, logN)) * TI + t] = v;
+    }
+    __syncthreads();
+    const int pairs = LO * (N / 2) * TI;
+    for (int h = 1; h < N; h <<= 1) {
+      const int stride = N / (2 * h);
+      for (int w = threadIdx.x; w < pairs; w += blockDim.x) {
+        int t = w % TI;
+        int j = (w / TI) % (N / 2);
+        int lo = w / (TI * (N / 2));
+        int q = j & (h - 1);
+        int a = ((j - q) << 1) + q;
+        int ia = (lo * N + a) * TI + t;
+        int ib = ia + h * TI;
+        uint32_t u = sm[ia];
+        uint32_t x = sm[ib];
+        uint32_t wv = tw[q * stride], wsv = tws[q * stride];
+        uint32_t v = shoup_mul(x, wv, wsv, p);
+        sm[ia] = add_mod(u, v, p);
+        sm[ib] = sub_mod(u, v, p);
+      }
+      __syncthreads();
+    }
+    for (int w = threadIdx.x; w < tile_words; w += blockDim.x) {
+      int t = w % TI;
+      int n = (w / TI) % N;
+      int lo = w / (TI * N);
+      int64_t oc = oc0 + lo;
+      if (oc < g.active_outer && t0 + t < g.inner) {
+        uint32_t v = sm[(lo * N + n) * TI + t];
+        if (INV && N > 1) v = shoup_mul(v, ninv, ninvs, p);
+        int64_t base = outer_offset(oc, g) * (int64_t)N * g.inner;
+        data[base + (int64_t)n * g.inner + t0 + t] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- global-memory fallback for very long axes (N > PDB_SMEM_NTT_MAX) -------
+__global__ void ntt_bitrev_global(uint32_t* __restrict__ data, AxisGeom g, int N, int logN) {
+  const int64_t lines = g.active_outer * g.inner;
+  const int64_t total = lines * (int64_t)N;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t line = w / N;
+    int n = (int)(w % N);
+    int rn = (int)bitrev((uint32_t)n, logN);
+    if (rn <= n) continue;
+    int64_t oc = line / g.inner, t = line % g.inner;
+    int64_t base = outer_offset(oc, g) * (int64_t)N * g.inner + t;
+    uint32_t a = data[base + (int64_t)n * g.inner];
+    uint32_t b = data[base + (int64_t)rn * g.inner];
+    data[base + (int64_t)n * g.inner] = b;
+    data[base + (int64_t)rn * g.inner] = a;
+  }
+}
+
+__global__ void ntt_stage_global(uint32_t* __restrict__ data, AxisGeom g, int N, int h,
+                                 const uint32_t* __restrict__ tw, const uint32_t* __restrict__ tws,
+                                 Mod32 m, int last, int inv, uint32_t ninv, uint32_t ninvs) {
+  const int64_t lines = g.active_outer * g.inner;
+  const int64_t total = lines * (int64_t)(N / 2);
+  const int stride = N / (2 * h);
+  const uint32_t p = m.p;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t line = w / (N / 2);
+    int j = (int)(w % (N / 2));
+    int64_t oc = line / g.inner, t = line % g.inner;
+    int64_t base = outer_offset(oc, g) * (int64_t)N * g.inner + t;
+    int q = j & (h - 1);
+    int a = ((j - q) << 1) + q;
+    int64_t ia = base + (int64_t)a * g.inner, ib = ia + (int64_t)h * g.inner;
+    uint32_t u = data[ia], x = data[ib];
+    uint32_t v = shoup_mul(x, tw[q * stride], tws[q * stride], p);
+    uint32_t ra = add_mod(u, v, p), rb = sub_mod(u, v, p);
+    if (last && inv) {
+      ra = shoup_mul(ra, ninv, ninvs, p);
+      rb = shoup_mul(rb, ninv, ninvs, p);
+    }
+    data[ia] = ra;
+    data[ib] = rb;
+  }
+}
+
+// Transform one axis of `batch` tensors of shape dims[0..nd) in place.
+// ext (may be null) gives, per dim, how many leading indices can be nonzero
+// on the dims before `axis` (lines outside that box are skipped).
+int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t* dims,
+             const int64_t* ext, int axis, bool inverse, cudaStream_t st) {
+  const int N = (int)dims[axis];
+  if (N == 1) return 0;  // length-1 transform is the identity (inverse scale 1)
+  const Twiddles* T = ctx_twiddles(ctx, N);
+  if (!T) return -1;
+  AxisGeom g;
+  g.inner = 1;
+  for (int d = axis + 1; d < nd; ++d) g.inner *= dims[d];
+  g.nbox = axis + 1;
+  g.box_dim[0] = batch;
+  g.box_ext[0] = batch;
+  for (int d = 0; d < axis; ++d) {
+    g.box_dim[d + 1] = dims[d];
+    g.box_ext[d + 1] = ext ? ext[d] : dims[d];
+  }
+  g.active_outer = 1;
+  for (int d = 0; d < g.nbox; ++d) g.active_outer *= g.box_ext[d];
+  if (g.active_outer == 0 || g.inner == 0) return 0;
+  const int logN = 31 - __builtin_clz((unsigned)N);
+  const uint32_t* tw = inverse ? T->inv : T->fwd;
+  const uint32_t* tws = inverse ? T->inv_s : T->fwd_s;
+  if (N <= PDB_SMEM_NTT_MAX) {
+    int TI = (int)(g.inner < 32 ? g.inner : 32);
+    while (TI > 1 && (int64_t)N * TI > PDB_SMEM_NTT_MAX) TI >>= 1;
+    int LO = 1;
+    while ((int64_t)LO * 2 * N * TI <= 4096 && LO * 2 <= g.active_outer) LO *= 2;
+    const int64_t tiles = ((g.active_outer + LO - 1) / LO) * ((g.inner + TI - 1) / TI);
+    const size_t smem = (size_t)LO * N * TI * sizeof(uint32_t);
+    int grid = (int)(tiles < (int64_t)ctx->sms * 16 ? tiles : (int64_t)ctx->sms * 16);
+    if (inverse)
+      ntt_axis_smem<true><<<grid, 256, smem, st>>>(data, g, N, logN, TI, LO, tw, tws, T->ninv, T->ninv_s, ctx->m);
+    else
+      ntt_axis_smem<false><<<grid, 256, smem, st>>>(data, g, N, logN, TI, LO, tw, tws, T->ninv, T->ninv_s, ctx->m);
+  } else {
+    const int64_t total = g.active_outer * g.inner * (int64_t)N;
+    int grid = (int)((total / 2 + 255) / 256);
+    if (grid > ctx->sms * 32) grid = ctx->sms * 32;
+    ntt_bitrev_global<<<grid, 256, 0, st>>>(data, g, N, logN);
+    for (int h = 1; h < N; h <<= 1)
+      ntt_stage_global<<<grid, 256, 0, st>>>(data, g, N, h, tw, tws, ctx->m, h == N / 2, inverse,
+                                             T->ninv, T->ninv_s);
+  }
+  return check_launch("ntt_axis");
+}
+
+}  // namespace pdb

@@ -1,0 +1,79 @@
+// Internal declarations shared by the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "modarith.cuh"
+
+#define PDB_MAX_DIMS 8
+#define PDB_SMEM_NTT_MAX 8192   // longest axis transformed in shared memory
+#define PDB_MAX_ORDER 64        // largest matrix order r
+#define PDB_MAX_PRIMES 256      // most primes in one CRT call
+
+namespace pdb {
+
+// Per-length twiddle tables of one prime (device memory).
+struct Twiddles {
+  int N = 0;
+  uint32_t* fwd = nullptr;    // w^j, j < N/2          (w = omega_N)
+  uint32_t* fwd_s = nullptr;  // Shoup companions
+  uint32_t* inv = nullptr;    // w^-j, j < N/2
+  uint32_t* inv_s = nullptr;
+  uint32_t* full = nullptr;   // w^c, c < N (node abscissae for fused evaluation)
+  uint32_t* full_s = nullptr;
+  uint32_t ninv = 1, ninv_s = 0;  // N^-1 and its companion
+};
+
+struct PrimeCtx {
+  uint64_t p = 0, omega = 0;
+  int q = 0;
+  Mod32 m;
+  int device = 0;
+  int sms = 148;
+  Twiddles tw[32];
+  std::mutex lock;
+};
+
+const Twiddles* ctx_twiddles(PrimeCtx* ctx, int N);
+
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t* dims,
+             const int64_t* ext, int axis, bool inverse, cudaStream_t st);
+
+// ---- entry sources for the determinant kernels ---------------------------------
+// Staged: materialised entry grids [k][stride] (node-major within an entry).
+struct StagedSrc {
+  const uint32_t* grids;
+  int64_t stride;
+  __device__ __forceinline__ uint32_t get(int e, int64_t node) const {
+    return __ldg(grids + (int64_t)e * stride + node);
+  }
+};
+
+// Fused: partially transformed entries [k][outer][E] (every axis but the last
+// already evaluated; E coefficient planes along the last axis).  The value of
+// entry e at node = o * NL + c is the degree-(E-1) polynomial in x = w_NL^c.
+struct FusedSrc {
+  const uint32_t* part;
+  int64_t outer;
+  int E;
+  int NL;
+  const uint32_t* xs;    // w^c, c < NL
+  const uint32_t* xss;   // companions
+  uint32_t p;
+  __device__ __forceinline__ uint32_t get(int e, int64_t node) const {
+    int64_t o = node / NL;
+    int c = (int)(node - o * NL);
+    const uint32_t* a = part + ((int64_t)e * outer + o) * E;
+    uint32_t x = __ldg(xs + c), xc = __ldg(xss + c);
+    uint32_t v = __ldg(a + E - 1);
+    for (int l = E - 2; l >= 0; --l) v = add_mod(shoup_mul(v, x, xc, p), __ldg(a + l), p);
+    return v;
+  }
+};
+
+}  // namespace pdb

@@ -1,0 +1,311 @@
+"""End-to-end GPU executor -- drop-in for the reference's `run`, `run_report`,
+`resume`, `resume_report` (pipeline.py:267-404).
+
+Per prime (all on one device, residues never leave HBM between stages):
+
+  FFT   reduce_scatter (coefficients -> padded residue grids)  +  pruned
+        multivariate NTT (pdb_ntt_multi_u32)             [_fft_stage 349-371]
+  DET   det mod p at every node (pdb_det_batch_u32)      [_det_stage 374-392]
+  IFFT  inverse multivariate NTT, in place               [_ifft_stage 395-404]
+
+then one CRT launch over the [P][nodes] residue block   [_execute 340-345].
+
+Two FFT/DET modes, same results:
+  * staged: every unique entry's grid is materialised ([k][nodes] u32), as in
+    the reference; required when a workspace must receive p{i}/fft/e{j}
+    artifacts, and used whenever the grids fit the memory budget.
+  * fused:  entries are transformed along all axes but the last and each
+    node's entries are evaluated inside the determinant kernel
+    (pdb_eval_det_fused_u32), so the k x nodes grid never exists (config C5:
+    1600 x 256^3 would be 107 GB per prime).  With a workspace, fused mode
+    checkpoints at p{i}/ifft granularity only (a reference `_execute` resumes
+    from such a workspace: it only consults has("p{i}/ifft")).
+
+Unit names, notification order, skip-if-stored and the workspace header
+logic follow the reference exactly, so kill/resume behaves identically.
+Stage timings are CUDA-event seconds of each stage's device work.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+
+from . import native
+from .checkpoint import Workspace, digest_of
+from .crt import device_lift
+from .errors import StaleWorkspaceError
+from .layout import CoeffTensor, PolyMatrix, residue_dtype
+from .planner import Plan, PipelineConfig, StageTimings, plan
+
+INPUT_FILE = "input.json"
+PLAN_FILE = "plan.json"
+
+#: staged grids above this many bytes switch to fused evaluation (override: PDB_STAGED_LIMIT)
+STAGED_LIMIT = int(os.environ.get("PDB_STAGED_LIMIT", str(8 << 30)))
+#: nodes per determinant launch in fused mode
+FUSED_CHUNK = 1 << 22
+
+
+# -- public API -------------------------------------------------------------------------
+
+def run(m: PolyMatrix, config: PipelineConfig = None, workspace=None) -> CoeffTensor:
+    """Exact signed-integer determinant of a polynomial matrix."""
+    return run_report(m, config, workspace)[0]
+
+
+def run_report(m: PolyMatrix, config: PipelineConfig = None, workspace=None):
+    """Like `run`, also returning (timings, plan)."""
+    cfg = config or PipelineConfig()
+    pl = plan(m, cfg)
+    ws = None
+    if workspace is not None:
+        ws = Workspace(workspace)
+        header = {"input_sha256": digest_of(m.to_dict()), "plan_sha256": pl.digest()}
+        if ws.exists():
+            if ws.open() != header:
+                raise StaleWorkspaceError(
+                    "stale workspace: manifest belongs to a different input or plan")
+        else:
+            ws.write_named(INPUT_FILE, m.to_dict())   # named files first: the manifest
+            ws.write_named(PLAN_FILE, pl.to_dict())   # is the commit point
+            ws.create(header)
+    result, timings = execute(m, pl, cfg, ws)
+    return result, timings, pl
+
+
+def resume(workspace, config: PipelineConfig = None) -> CoeffTensor:
+    """Continue (or just reload) a checkpointed run."""
+    return resume_report(workspace, config)[0]
+
+
+def resume_report(workspace, config: PipelineConfig = None):
+    cfg = config or PipelineConfig()
+    ws = Workspace(workspace)
+    header = ws.open()
+    ws.verify()
+    m = PolyMatrix.from_dict(ws.read_named(INPUT_FILE))
+    pl = Plan.from_dict(ws.read_named(PLAN_FILE))
+    if (header.get("input_sha256") != digest_of(m.to_dict())
+            or header.get("plan_sha256") != pl.digest()):
+        raise StaleWorkspaceError("stale workspace: stored input or plan was altered")
+    result, timings = execute(m, pl, cfg, ws)
+    return result, timings, pl
+
+
+# -- host preparation -----------------------------------------------------------------------
+
+def _limbs_of(values):
+    """Signed Python ints -> (magnitude limbs [n][L] u32, negative flags, L)."""
+    vals = list(values)
+    if not vals:
+        return np.zeros((0, 1), dtype=np.uint32), np.zeros(0, dtype=np.uint8), 1
+    top = max(abs(v) for v in vals)
+    L = max(1, (top.bit_length() + 31) // 32)
+    neg = np.fromiter((v < 0 for v in vals), dtype=np.uint8, count=len(vals))
+    if L <= 2:
+        mag = np.array([abs(v) for v in vals], dtype=np.uint64)
+        limbs = np.stack([(mag & 0xFFFFFFFF).astype(np.uint32), (mag >> 32).astype(np.uint32)], axis=1)[:, :L]
+    else:
+        raw = b"".join(abs(v).to_bytes(4 * L, "little") for v in vals)
+        limbs = np.frombuffer(raw, dtype="<u4").reshape(len(vals), L)
+    return np.ascontiguousarray(limbs, dtype=np.uint32), neg, L
+
+
+class DevicePlan:
+    """Everything uploaded once per run: coefficient limbs, scatter positions
+    for both layouts, entry ids; plus the mode decision."""
+
+    def __init__(self, m: PolyMatrix, pl: Plan, device, staged: bool):
+        torch = native._torch()
+        self.m, self.pl, self.device = m, pl, device
+        self.shape = tuple(pl.shape)
+        self.vn = len(self.shape)
+        self.nodes = pl.node_count
+        self.k = m.k
+        self.staged = staged or self.vn == 0
+        entries, coeffs = [], []
+        for e, t in enumerate(m.unique_entries):
+            for exps, c in t.terms().items():
+                entries.append((e, exps))
+                coeffs.append(c)
+        mag, neg, L = _limbs_of(coeffs)
+        self.count = len(coeffs)
+        self.L = L
+        if self.staged:
+            pos = [e * self.nodes + _flat(exps, self.shape) for e, exps in entries]
+        else:
+            self.E = max(t.shape[-1] for t in m.unique_entries)
+            self.outer = self.nodes // self.shape[-1]
+            pos = [(e * self.outer + _flat(exps[:-1], self.shape[:-1])) * self.E + exps[-1]
+                   for e, exps in entries]
+        self.mag = torch.from_numpy(mag.view(np.int32).copy()).to(device) if self.count else \
+            torch.zeros(1, dtype=torch.int32, device=device)
+        self.neg = torch.from_numpy(neg.copy()).to(device) if self.count else \
+            torch.zeros(1, dtype=torch.uint8, device=device)
+        self.pos = torch.tensor(pos if pos else [0], dtype=torch.int64, device=device)
+        self.ids = torch.tensor(list(m.entry_ids), dtype=torch.int32, device=device)
+        # per-axis coefficient extents (for NTT pruning): largest exponent + 1
+        self.ext = [max(t.shape[a] for t in m.unique_entries) for a in range(self.vn)]
+
+    def buffer_words(self) -> int:
+        return self.k * self.nodes if self.staged else self.k * self.outer * self.E
+
+
+def _flat(exps, shape):
+    pos = 0
+    for e, n in zip(exps, shape):
+        pos = pos * n + e
+    return pos
+
+
+def choose_staged(m: PolyMatrix, pl: Plan, ws) -> bool:
+    if len(pl.shape) == 0:
+        return True
+    grid_bytes = 4 * m.k * pl.node_count
+    if ws is not None and grid_bytes <= STAGED_LIMIT:
+        return True
+    return grid_bytes <= STAGED_LIMIT and pl.r <= 8 or grid_bytes <= STAGED_LIMIT // 4
+
+
+# -- the executor ------------------------------------------------------------------------
+
+class _Timer:
+    def __init__(self, torch, stream):
+        self.torch, self.stream = torch, stream
+        self.marks = []
+
+    def mark(self):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record(self.stream)
+        self.marks.append(ev)
+        return ev
+
+
+def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws, primes_subset=None):
+    """Run the per-prime stages and the CRT (reference `_execute`, pipeline.py:323-346)."""
+    timings = StageTimings()
+    if ws is not None and ws.has("crt"):
+        return _tensor_from_payload(ws.load_json("crt")), timings
+    torch = native._torch()
+    device = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+    staged = choose_staged(m, pl, ws)
+    dp = DevicePlan(m, pl, device, staged)
+    nodes = dp.nodes
+    P = pl.prime_count
+    residues = torch.empty((P, nodes), dtype=torch.int32, device=device)
+    work = torch.empty(dp.buffer_words() or 1, dtype=torch.int32, device=device)
+    det_chunk = nodes if dp.staged else min(nodes, FUSED_CHUNK)
+    det_buf = torch.empty(nodes, dtype=torch.int32, device=device)
+    scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, det_chunk), device)
+    events = []   # (stage, start, end)
+    for pi, spec in enumerate(pl.primes):
+        unit = "p%d/ifft" % pi
+        if ws is not None and ws.has(unit):
+            residues[pi].copy_(native.to_device_u32(_load_grid(ws, unit, pl)))
+            continue
+        ctx = native.prime_context(spec, device.index)
+        t0 = _Timer(torch, stream).mark()
+        _fft_stage(dp, ctx, work, ws, pi, cfg)
+        t1 = _Timer(torch, stream).mark()
+        _det_stage(dp, ctx, work, det_buf, scratch, det_chunk, ws, pi, cfg)
+        t2 = _Timer(torch, stream).mark()
+        residues[pi].copy_(det_buf)
+        native.ntt_multi(ctx, residues[pi], 1, dp.shape, None, range(dp.vn), True)
+        t3 = _Timer(torch, stream).mark()
+        events.append((t0, t1, t2, t3))
+        if ws is not None:
+            ws.store_residues(unit, native.to_host_u32(residues[pi]), pl.shape)
+        cfg._notify(unit)
+    t4 = _Timer(torch, stream).mark()
+    coeffs = device_lift(residues, [s.p for s in pl.primes], nodes, nodes)
+    t5 = _Timer(torch, stream).mark()
+    torch.cuda.synchronize()
+    for t0, t1, t2, t3 in events:
+        timings.fft += t0.elapsed_time(t1) / 1e3
+        timings.det += t1.elapsed_time(t2) / 1e3
+        timings.ifft += t2.elapsed_time(t3) / 1e3
+    timings.crt += t4.elapsed_time(t5) / 1e3
+    result = CoeffTensor(tuple(pl.shape), tuple(coeffs), tuple(pl.variables))
+    if ws is not None:
+        ws.store_json("crt", _payload_from_tensor(result))
+    cfg._notify("crt")
+    return result, timings
+
+
+def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
+    """Entry grids of one prime: reduce + scatter + pruned NTT (staged or partial)."""
+    m, pl = dp.m, dp.pl
+    work.zero_()
+    if not dp.staged:
+        native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, work)
+        dims = dp.shape[:-1] + (dp.E,)
+        ext = dp.ext[:-1] + [dp.E]
+        native.ntt_multi(ctx, work, dp.k, dims, ext, range(dp.vn - 1), False)
+        return
+    todo = []
+    for eid in range(dp.k):
+        unit = "p%d/fft/e%d" % (pi, eid)
+        if ws is not None and ws.has(unit):
+            grid = _load_grid(ws, unit, pl)
+            work[eid * dp.nodes:(eid + 1) * dp.nodes].copy_(native.to_device_u32(grid))
+        else:
+            todo.append(eid)
+    if not todo:
+        return
+    if len(todo) < dp.k:
+        # keep stored grids: scatter into a side buffer and transform only the todo entries
+        native._torch()
+        fresh = work.new_zeros(dp.k * dp.nodes)
+        native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, fresh)
+        for eid in todo:
+            sl = fresh[eid * dp.nodes:(eid + 1) * dp.nodes]
+            native.ntt_multi(ctx, sl, 1, dp.shape, dp.ext, range(dp.vn), False)
+            work[eid * dp.nodes:(eid + 1) * dp.nodes].copy_(sl)
+    else:
+        native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, work)
+        native.ntt_multi(ctx, work, dp.k, dp.shape, dp.ext, range(dp.vn), False)
+    for eid in todo:
+        unit = "p%d/fft/e%d" % (pi, eid)
+        if ws is not None:
+            ws.store_residues(unit, native.to_host_u32(work[eid * dp.nodes:(eid + 1) * dp.nodes]), pl.shape)
+        cfg._notify(unit)
+
+
+def _det_stage(dp: DevicePlan, ctx, work, det_buf, scratch, chunk, ws, pi, cfg):
+    pl = dp.pl
+    unit = "p%d/det" % pi
+    if ws is not None and ws.has(unit):
+        det_buf.copy_(native.to_device_u32(_load_grid(ws, unit, pl)))
+        return
+    if dp.staged:
+        native.det_batch(ctx, work, dp.nodes, dp.ids, pl.r, 0, dp.nodes, det_buf, scratch)
+    else:
+        n_last = dp.shape[-1]
+        for lo in range(0, dp.nodes, chunk):
+            cnt = min(chunk, dp.nodes - lo)
+            native.eval_det_fused(ctx, work, dp.outer, dp.E, n_last, dp.ids, pl.r, lo, cnt,
+                                  det_buf[lo:lo + cnt], scratch)
+    if dp.staged:   # fused mode has no det (or fft) units: it checkpoints per prime
+        if ws is not None:
+            ws.store_residues(unit, native.to_host_u32(det_buf), pl.shape)
+        cfg._notify(unit)
+
+
+def _load_grid(ws, unit, pl):
+    values, shape = ws.load_array(unit)
+    if tuple(shape) != tuple(pl.shape):
+        raise StaleWorkspaceError("stale workspace: artifact shape %s != %s" % (shape, pl.shape))
+    return values
+
+
+def _payload_from_tensor(t: CoeffTensor) -> dict:
+    return {"variables": list(t.axis_vars), "shape": list(t.shape), "coeffs": list(t.coeffs)}
+
+
+def _tensor_from_payload(payload) -> CoeffTensor:
+    return CoeffTensor(tuple(payload["shape"]), tuple(int(c) for c in payload["coeffs"]),
+                       tuple(payload["variables"]))

@@ -1,0 +1,240 @@
+"""ctypes binding of libpolydet_b200.so (the C ABI in include/polydet_b200.h).
+
+The library is the ONLY compute path of this package: if it is missing, or
+no CUDA device is visible, every call raises DeviceError -- there is no CPU
+fallback.  torch is used purely for device memory and streams: tensors are
+allocated with torch and handed to the kernels as raw pointers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import DeviceError
+
+LIB_NAME = "libpolydet_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+U32_LIMIT = 2**31  # device kernels: p < 2^31
+
+_lib = None
+_lock = threading.Lock()
+
+_c_i32, _c_i64, _c_u32, _c_u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
+_c_size, _c_vp = ctypes.c_size_t, ctypes.c_void_p
+
+_SIGNATURES = {
+    "pdb_last_error": (ctypes.c_char_p, []),
+    "pdb_version": (_c_i32, []),
+    "pdb_device_sm_count": (_c_i32, [_c_i32]),
+    "pdb_prime_ctx_create": (_c_i32, [_c_u64, _c_u64, _c_i32, ctypes.POINTER(_c_vp)]),
+    "pdb_prime_ctx_destroy": (_c_i32, [_c_vp]),
+    "pdb_prime_ctx_prepare": (_c_i32, [_c_vp, _c_i64]),
+    "pdb_ntt_multi_u32": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp, _c_u32, _c_i32, _c_vp]),
+    "pdb_reduce_scatter_u32": (_c_i32, [_c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp]),
+    "pdb_det_scratch_bytes": (_c_size, [_c_i32, _c_i64]),
+    "pdb_det_batch_u32": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i32, _c_i64, _c_i64, _c_vp,
+                                   _c_vp, _c_size, _c_vp]),
+    "pdb_eval_det_fused_u32": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_vp, _c_i32, _c_i64,
+                                        _c_i64, _c_vp, _c_vp, _c_size, _c_vp]),
+    "pdb_condense_u32": (_c_i32, [_c_vp, _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_vp, _c_size, _c_vp]),
+    "pdb_crt_limbs": (_c_i32, [_c_i32]),
+    "pdb_crt_scratch_bytes": (_c_size, [_c_i32]),
+    "pdb_crt_mrc_u32": (_c_i32, [_c_vp, _c_i32, _c_i64, _c_i64, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp,
+                                 _c_size, _c_vp]),
+    "pdb_mulmod_peak": (_c_i32, [_c_u32, _c_i32, ctypes.POINTER(ctypes.c_double), _c_vp]),
+}
+
+
+def exported_symbols():
+    """Names the header declares (checked by the CPU test suite)."""
+    return sorted(_SIGNATURES)
+
+
+def load_library():
+    """Load (once) and type the shared library; raise DeviceError if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = os.environ.get("PDB_LIBRARY", str(LIB_PATH))
+        if not Path(path).is_file():
+            raise DeviceError(
+                "%s not built (run __graft_entry__.build() or `make -C "
+                "paper_2010_12117_b200/csrc`); there is no CPU fallback" % path)
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the determinant pipeline runs only on the GPU")
+    return torch
+
+
+def check(rc: int, what: str = ""):
+    if rc == 0:
+        return
+    msg = load_library().pdb_last_error().decode(errors="replace")
+    if rc == -2:
+        raise ValueError(msg)
+    raise DeviceError("%s failed: %s" % (what or "kernel", msg))
+
+
+def stream_handle(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def host_i64(values) -> ctypes.Array:
+    vals = [int(v) for v in values]
+    return (ctypes.c_int64 * max(len(vals), 1))(*vals)
+
+
+class PrimeContext:
+    """Device twiddle tables + constants of one prime (reference TwiddleTable)."""
+
+    def __init__(self, p: int, omega: int, q: int, device: int):
+        if p >= U32_LIMIT:
+            raise ValueError("modulus %d exceeds the 32-bit device kernels (p < 2^31)" % p)
+        lib = load_library()
+        torch = _torch()
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            check(lib.pdb_prime_ctx_create(p, omega, q, ctypes.byref(handle)), "prime context")
+        self.handle = handle
+        self.p, self.omega, self.q, self.device = p, omega, q, device
+        self._lib = lib
+
+    def prepare(self, n: int):
+        import torch
+        with torch.cuda.device(self.device):
+            check(self._lib.pdb_prime_ctx_prepare(self.handle, int(n)), "twiddle tables")
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self._lib.pdb_prime_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_contexts: dict = {}
+
+
+def prime_context(spec, device=None) -> PrimeContext:
+    torch = _torch()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    key = (spec.p, spec.omega, spec.q, dev)
+    with _lock:
+        ctx = _contexts.get(key)
+    if ctx is None:
+        ctx = PrimeContext(spec.p, spec.omega, spec.q, dev)
+        with _lock:
+            _contexts[key] = ctx
+    return ctx
+
+
+# -- thin typed wrappers (device tensors in, nothing returned) ------------------------
+
+def ntt_multi(ctx: PrimeContext, data, batch: int, dims, extents, axes, inverse: bool, stream=None):
+    lib = load_library()
+    nd = len(dims)
+    mask = 0
+    for a in axes:
+        mask |= 1 << a
+    ext = host_i64(extents) if extents is not None else None
+    check(lib.pdb_ntt_multi_u32(ctx.handle, ptr(data), int(batch), nd, host_i64(dims),
+                                ext, mask, int(bool(inverse)), stream_handle(stream)), "ntt")
+
+
+def reduce_scatter(ctx: PrimeContext, mag, neg, pos, count: int, limbs: int, dst, stream=None):
+    lib = load_library()
+    check(lib.pdb_reduce_scatter_u32(ctx.handle, ptr(mag), ptr(neg), ptr(pos), int(count), int(limbs),
+                                     ptr(dst), stream_handle(stream)), "reduce_scatter")
+
+
+def det_scratch_bytes(r: int, nodes: int) -> int:
+    return int(load_library().pdb_det_scratch_bytes(int(r), int(nodes)))
+
+
+def det_batch(ctx: PrimeContext, grids, grid_stride: int, ids, r: int, node_lo: int, nodes: int,
+              out, scratch, stream=None):
+    lib = load_library()
+    check(lib.pdb_det_batch_u32(ctx.handle, ptr(grids), int(grid_stride), ptr(ids), int(r), int(node_lo),
+                                int(nodes), ptr(out), ptr(scratch), scratch.numel() * scratch.element_size(),
+                                stream_handle(stream)), "det")
+
+
+def eval_det_fused(ctx: PrimeContext, partial, outer: int, ncoef: int, n_last: int, ids, r: int,
+                   node_lo: int, nodes: int, out, scratch, stream=None):
+    lib = load_library()
+    check(lib.pdb_eval_det_fused_u32(ctx.handle, ptr(partial), int(outer), int(ncoef), int(n_last),
+                                     ptr(ids), int(r), int(node_lo), int(nodes), ptr(out), ptr(scratch),
+                                     scratch.numel() * scratch.element_size(), stream_handle(stream)),
+          "fused det")
+
+
+def condense(ctx: PrimeContext, mat, r: int, trail_vals, trail_cols, det_out, scratch, stream=None):
+    lib = load_library()
+    check(lib.pdb_condense_u32(ctx.handle, ptr(mat), int(r), ptr(trail_vals), ptr(trail_cols),
+                               ptr(det_out), ptr(scratch), scratch.numel() * scratch.element_size(),
+                               stream_handle(stream)), "condense")
+
+
+def crt_limbs(nprimes: int) -> int:
+    return int(load_library().pdb_crt_limbs(int(nprimes)))
+
+
+def crt_scratch_bytes(nprimes: int) -> int:
+    return int(load_library().pdb_crt_scratch_bytes(int(nprimes)))
+
+
+def crt_mrc(residues, nprimes: int, n: int, stride: int, primes, limbs, L: int, neg, scratch, stream=None):
+    lib = load_library()
+    hp = (ctypes.c_uint32 * nprimes)(*[int(p) for p in primes])
+    check(lib.pdb_crt_mrc_u32(ptr(residues), int(nprimes), int(n), int(stride), hp, ptr(limbs), int(L),
+                              ptr(neg), ptr(scratch), scratch.numel() * scratch.element_size(),
+                              stream_handle(stream)), "crt")
+
+
+def mulmod_peak(p: int, variant: int) -> float:
+    lib = load_library()
+    _torch()
+    out = ctypes.c_double()
+    check(lib.pdb_mulmod_peak(int(p), int(variant), ctypes.byref(out), stream_handle()), "peak")
+    return out.value
+
+
+# -- host <-> device helpers ---------------------------------------------------------
+
+def to_device_u32(values, device=None):
+    """numpy residues (any int dtype, values < 2^32) -> int32-typed device tensor."""
+    torch = _torch()
+    arr = np.ascontiguousarray(np.asarray(values).astype(np.uint32, copy=False)).view(np.int32)
+    return torch.from_numpy(arr).to(device or torch.cuda.current_device())
+
+
+def to_host_u32(t) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint32)
+
+
+def scratch_tensor(nbytes: int, device=None):
+    torch = _torch()
+    words = max((int(nbytes) + 15) // 16 * 4, 4)
+    return torch.empty(words, dtype=torch.int32, device=device or torch.cuda.current_device())
