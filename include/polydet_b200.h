@@ -40,6 +40,8 @@ typedef struct pdb_prime_ctx pdb_prime_ctx;
 
 const char* pdb_last_error(void);
 int32_t pdb_version(void);
+/* Kernels launched by this library since load (process-wide counter). */
+int64_t pdb_launch_count(void);
 int32_t pdb_device_sm_count(int32_t device);
 
 /* Prime p = c * 2^q + 1 with omega of exact order 2^q (reference PrimeSpec,

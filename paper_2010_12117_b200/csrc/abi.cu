@@ -1,4 +1,5 @@
 // extern "C" boundary of libpolydet_b200.so (declared in include/polydet_b200.h).
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <vector>
@@ -12,6 +13,9 @@ struct pdb_prime_ctx : pdb::PrimeCtx {};
 namespace pdb {
 
 static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -169,6 +173,7 @@ extern "C" {
 
 const char* pdb_last_error(void) { return g_err; }
 int32_t pdb_version(void) { return 1; }
+int64_t pdb_launch_count(void) { return g_launches.load(); }
 
 int32_t pdb_device_sm_count(int32_t device) {
   int v = 0;

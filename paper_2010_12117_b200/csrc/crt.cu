@@ -94,6 +94,7 @@ int reduce_scatter(PrimeCtx* ctx, const uint32_t* mag, const uint8_t* neg, const
   int64_t blocks = (count + 255) / 256;
   int grid = (int)(blocks < (int64_t)ctx->sms * 8 ? blocks : (int64_t)ctx->sms * 8);
   reduce_scatter_kernel<<<grid, 256, 0, st>>>(mag, neg, pos, count, Lc, dst, ctx->m);
+  count_launch();
   return check_launch("reduce_scatter");
 }
 
@@ -180,6 +181,7 @@ int crt_mrc(const uint32_t* res, int P, int64_t n, int64_t res_stride, const uin
     int64_t blocks = (n + 127) / 128;
     int grid = (int)(blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16);
     crt_mrc_kernel<<<grid, 128, 0, st>>>(res, P, n, res_stride, d_cp, d_w, d_ws, d_prod, L, limbs, neg);
+    count_launch();
   }
   return check_launch("crt_mrc");
 }

@@ -126,7 +126,7 @@ template <class Src>
 static int launch_small(int r, Src src, const int32_t* ids, int64_t lo, int64_t n, uint32_t* out,
                         FlagList f, Mod32 m, int grid, cudaStream_t st) {
   switch (r) {
-#define PDB_SMALL(R) case R: det_small<R, Src><<<grid, 128, 0, st>>>(src, ids, lo, n, out, f, m); break;
+#define PDB_SMALL(R) case R: det_small<R, Src><<<grid, 128, 0, st>>>(src, ids, lo, n, out, f, m); count_launch(); break;
     PDB_SMALL(1) PDB_SMALL(2) PDB_SMALL(3) PDB_SMALL(4)
     PDB_SMALL(5) PDB_SMALL(6) PDB_SMALL(7) PDB_SMALL(8)
 #undef PDB_SMALL
@@ -180,9 +180,11 @@ int det_run(PrimeCtx* ctx, Src src, const int32_t* ids, int r, int64_t node_lo, 
   if (fast) {
     det_robust<Src><<<slots / 128, 128, 0, st>>>(src, ids, r, flags.nodes, flags.count, 0, node_lo,
                                                   out, mats, m);
+    count_launch();
   } else {
     det_robust<Src><<<slots / 128, 128, 0, st>>>(src, ids, r, nullptr, nullptr, nodes, node_lo,
                                                   out, mats, m);
+    count_launch();
   }
   return check_launch("det_robust");
 }
@@ -208,6 +210,7 @@ int condense_run(PrimeCtx* ctx, const uint32_t* mat, int r, uint32_t* trail_vals
   StagedSrc src{mat, 1};
   det_robust<StagedSrc><<<1, 128, 0, st>>>(src, d_ids, r, nullptr, nullptr, 1, 0, det_out, mats, ctx->m,
                                            trail_vals, trail_cols);
+  count_launch();
   return check_launch("condense");
 }
 

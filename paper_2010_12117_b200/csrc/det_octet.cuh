@@ -167,44 +167,41 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
       }
       __syncwarp(omask);
       // ---------------- trailing rows (lanes split rows) ----------------
-      const int c0 = K + Bk;
+      // Trailing rows exist only when r - K > B, i.e. for full blocks (Bk == OCT_B),
+      // so everything below is unrolled over the compile-time block size.
+      const int c0 = K + OCT_B;
       const int cend = (r + 3) & ~3;
-      const uint32_t zpr = ZPR[Bk];
+      const uint32_t zpr = ZPR[OCT_B];
+      const uint32_t* npr = A + K * S;                  // NPR_q[c] = npr[q * S + c]
       for (int i = c0 + l; i < r; i += OCT_LPM) {
+        uint32_t* row = A + i * S;
         uint32_t t[OCT_B], tau[OCT_B];
 #pragma unroll
         for (int q = 0; q < OCT_B; ++q) {
-          if (q < Bk) {
-            uint64_t acc = (uint64_t)A[i * S + K + q] * ZPR[q];
+          uint64_t acc = mad_wide(row[K + q], ZPR[q], 0ull);
 #pragma unroll
-            for (int s2 = 0; s2 < OCT_B; ++s2)
-              if (s2 < q) acc += (uint64_t)t[s2] * V[s2 * OCT_B + q];
-            t[q] = oct_reduce(acc, m);
-            tau[q] = shoup_mul(t[q], ZETA[q], ZETAs[q], p);
-          } else {
-            tau[q] = 0;
-          }
+          for (int s2 = 0; s2 < q; ++s2) acc = mad_wide(t[s2], V[s2 * OCT_B + q], acc);
+          t[q] = oct_reduce(acc, m);
+          tau[q] = shoup_mul(t[q], ZETA[q], ZETAs[q], p);
         }
         for (int c = c0; c < cend; c += 4) {
-          const uint4 a4 = *reinterpret_cast<const uint4*>(A + i * S + c);
-          uint64_t a0 = (uint64_t)a4.x * zpr, a1 = (uint64_t)a4.y * zpr;
-          uint64_t a2 = (uint64_t)a4.z * zpr, a3 = (uint64_t)a4.w * zpr;
+          const uint4 a4 = *reinterpret_cast<const uint4*>(row + c);
+          uint64_t a0 = mad_wide(a4.x, zpr, 0ull), a1 = mad_wide(a4.y, zpr, 0ull);
+          uint64_t a2 = mad_wide(a4.z, zpr, 0ull), a3 = mad_wide(a4.w, zpr, 0ull);
 #pragma unroll
           for (int q = 0; q < OCT_B; ++q) {
-            if (q < Bk) {
-              const uint4 n4 = *reinterpret_cast<const uint4*>(A + (K + q) * S + c);
-              a0 += (uint64_t)tau[q] * n4.x;
-              a1 += (uint64_t)tau[q] * n4.y;
-              a2 += (uint64_t)tau[q] * n4.z;
-              a3 += (uint64_t)tau[q] * n4.w;
-            }
+            const uint4 n4 = *reinterpret_cast<const uint4*>(npr + q * S + c);
+            a0 = mad_wide(tau[q], n4.x, a0);
+            a1 = mad_wide(tau[q], n4.y, a1);
+            a2 = mad_wide(tau[q], n4.z, a2);
+            a3 = mad_wide(tau[q], n4.w, a3);
           }
           uint4 o;
           o.x = oct_reduce(a0, m);
           o.y = oct_reduce(a1, m);
           o.z = oct_reduce(a2, m);
           o.w = oct_reduce(a3, m);
-          *reinterpret_cast<uint4*>(A + i * S + c) = o;
+          *reinterpret_cast<uint4*>(row + c) = o;
         }
       }
       __syncwarp(omask);
@@ -251,6 +248,7 @@ int launch_octet(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int64_t node
   int grid = (int)(ctas < cap ? ctas : cap);
   det_octet_kernel<Src><<<grid, warps * 32, smem, st>>>(src, ids, node_lo, nodes, out, flag_count,
                                                         flag_nodes, g, ctx->m);
+  count_launch();
   return check_launch("det_octet");
 }
 

@@ -84,6 +84,17 @@ PDB_HD uint32_t mul_mod(uint32_t a, uint32_t b, const Mod32& m) {
   return csub((uint32_t)r, m.p);
 }
 
+// c + a*b as one IMAD.WIDE.U32 (64-bit accumulate of a 32x32 product).
+PDB_HD uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c) {
+#ifdef __CUDA_ARCH__
+  uint64_t d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+#else
+  return c + (uint64_t)a * b;
+#endif
+}
+
 // Montgomery reduction: returns v == acc * 2^-32 (mod p) with v < 2^32,
 // valid whenever acc < (2^32 - p - 1) * 2^32 (e.g. <= 12 products of residues
 // when p < 2^30).

@@ -190,6 +190,7 @@ int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t
       ntt_axis_smem<true><<<grid, 256, smem, st>>>(data, g, N, logN, TI, LO, tw, tws, T->ninv, T->ninv_s, ctx->m);
     else
       ntt_axis_smem<false><<<grid, 256, smem, st>>>(data, g, N, logN, TI, LO, tw, tws, T->ninv, T->ninv_s, ctx->m);
+    count_launch();  // one launch on either branch
   } else {
     const int64_t total = g.active_outer * g.inner * (int64_t)N;
     int grid = (int)((total / 2 + 255) / 256);
@@ -198,6 +199,7 @@ int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t
     for (int h = 1; h < N; h <<= 1)
       ntt_stage_global<<<grid, 256, 0, st>>>(data, g, N, h, tw, tws, ctx->m, h == N / 2, inverse,
                                              T->ninv, T->ninv_s);
+    count_launch(1 + logN);
   }
   return check_launch("ntt_axis");
 }

@@ -40,6 +40,8 @@ const Twiddles* ctx_twiddles(PrimeCtx* ctx, int N);
 
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
+// Counts kernel launches issued by this library (pdb_launch_count()).
+void count_launch(long long n = 1);
 
 int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t* dims,
              const int64_t* ext, int axis, bool inverse, cudaStream_t st);

@@ -33,7 +33,7 @@ import os
 
 import numpy as np
 
-from . import native
+from . import native, shard
 from .checkpoint import Workspace, digest_of
 from .crt import device_lift
 from .errors import StaleWorkspaceError
@@ -161,9 +161,15 @@ def _flat(exps, shape):
     return pos
 
 
+#: None = automatic; "staged" / "fused" force a mode (tests, benchmarks)
+FORCE_MODE = None
+
+
 def choose_staged(m: PolyMatrix, pl: Plan, ws) -> bool:
     if len(pl.shape) == 0:
         return True
+    if FORCE_MODE is not None and ws is None:
+        return FORCE_MODE == "staged"
     grid_bytes = 4 * m.k * pl.node_count
     if ws is not None and grid_bytes <= STAGED_LIMIT:
         return True
@@ -184,28 +190,38 @@ class _Timer:
         return ev
 
 
-def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws, primes_subset=None):
-    """Run the per-prime stages and the CRT (reference `_execute`, pipeline.py:323-346)."""
+def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
+    """Run the per-prime stages and the CRT (reference `_execute`, pipeline.py:323-346).
+
+    Under torch.distributed with world size G > 1 (one process per GPU), rank
+    g computes primes g, g+G, ... and the residue blocks are all-gathered
+    (NCCL) before the CRT; every rank returns the same result.
+    """
     timings = StageTimings()
     if ws is not None and ws.has("crt"):
         return _tensor_from_payload(ws.load_json("crt")), timings
     torch = native._torch()
+    rank, size = shard.world()
+    if size > 1 and ws is not None:
+        raise ValueError("workspace checkpointing runs on a single device (world size %d)" % size)
     device = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream()
     staged = choose_staged(m, pl, ws)
     dp = DevicePlan(m, pl, device, staged)
     nodes = dp.nodes
     P = pl.prime_count
-    residues = torch.empty((P, nodes), dtype=torch.int32, device=device)
+    mine = shard.my_primes(P, rank, size)
+    residues = torch.empty((len(mine), nodes), dtype=torch.int32, device=device)
     work = torch.empty(dp.buffer_words() or 1, dtype=torch.int32, device=device)
     det_chunk = nodes if dp.staged else min(nodes, FUSED_CHUNK)
     det_buf = torch.empty(nodes, dtype=torch.int32, device=device)
     scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, det_chunk), device)
-    events = []   # (stage, start, end)
-    for pi, spec in enumerate(pl.primes):
+    events = []
+    for row, pi in enumerate(mine):
+        spec = pl.primes[pi]
         unit = "p%d/ifft" % pi
         if ws is not None and ws.has(unit):
-            residues[pi].copy_(native.to_device_u32(_load_grid(ws, unit, pl)))
+            residues[row].copy_(native.to_device_u32(_load_grid(ws, unit, pl)))
             continue
         ctx = native.prime_context(spec, device.index)
         t0 = _Timer(torch, stream).mark()
@@ -213,13 +229,15 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws, primes_subset=None
         t1 = _Timer(torch, stream).mark()
         _det_stage(dp, ctx, work, det_buf, scratch, det_chunk, ws, pi, cfg)
         t2 = _Timer(torch, stream).mark()
-        residues[pi].copy_(det_buf)
-        native.ntt_multi(ctx, residues[pi], 1, dp.shape, None, range(dp.vn), True)
+        residues[row].copy_(det_buf)
+        native.ntt_multi(ctx, residues[row], 1, dp.shape, None, range(dp.vn), True)
         t3 = _Timer(torch, stream).mark()
         events.append((t0, t1, t2, t3))
         if ws is not None:
-            ws.store_residues(unit, native.to_host_u32(residues[pi]), pl.shape)
+            ws.store_residues(unit, native.to_host_u32(residues[row]), pl.shape)
         cfg._notify(unit)
+    if size > 1:
+        residues = shard.gather_residues(residues, P, rank, size)
     t4 = _Timer(torch, stream).mark()
     coeffs = device_lift(residues, [s.p for s in pl.primes], nodes, nodes)
     t5 = _Timer(torch, stream).mark()
@@ -309,3 +327,45 @@ def _payload_from_tensor(t: CoeffTensor) -> dict:
 def _tensor_from_payload(payload) -> CoeffTensor:
     return CoeffTensor(tuple(payload["shape"]), tuple(int(c) for c in payload["coeffs"]),
                        tuple(payload["variables"]))
+
+
+# -- stage-level access (tests, benchmarks) ---------------------------------------------
+
+class PrimeStages:
+    """Device buffers + one prime's FWD/DET/INV, reusable across primes and steps.
+
+    `forward(pi)` builds the entry grids (staged) or the partial transform
+    (fused); `determinants(pi)` fills `det` for every node; `interpolate(pi)`
+    turns `det` into the residue tensor in place.  Used by bench.py to time
+    exactly the per-prime hot path and by the tests to replay stages.
+    """
+
+    def __init__(self, m: PolyMatrix, pl: Plan, staged: bool):
+        torch = native._torch()
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.m, self.pl = m, pl
+        self.dp = DevicePlan(m, pl, self.device, staged)
+        dp = self.dp
+        self.work = torch.empty(dp.buffer_words() or 1, dtype=torch.int32, device=self.device)
+        self.chunk = dp.nodes if dp.staged else min(dp.nodes, FUSED_CHUNK)
+        self.det = torch.empty(dp.nodes, dtype=torch.int32, device=self.device)
+        self.scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, self.chunk), self.device)
+        self._cfg = PipelineConfig()
+
+    def ctx(self, pi):
+        return native.prime_context(self.pl.primes[pi], self.device.index)
+
+    def forward(self, pi):
+        _fft_stage(self.dp, self.ctx(pi), self.work, None, pi, self._cfg)
+
+    def determinants(self, pi):
+        _det_stage(self.dp, self.ctx(pi), self.work, self.det, self.scratch, self.chunk, None, pi, self._cfg)
+
+    def interpolate(self, pi):
+        native.ntt_multi(self.ctx(pi), self.det, 1, self.dp.shape, None, range(self.dp.vn), True)
+
+    def step(self, pi):
+        self.forward(pi)
+        self.determinants(pi)
+        self.interpolate(pi)

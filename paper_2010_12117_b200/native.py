@@ -30,6 +30,7 @@ _c_size, _c_vp = ctypes.c_size_t, ctypes.c_void_p
 _SIGNATURES = {
     "pdb_last_error": (ctypes.c_char_p, []),
     "pdb_version": (_c_i32, []),
+    "pdb_launch_count": (_c_i64, []),
     "pdb_device_sm_count": (_c_i32, [_c_i32]),
     "pdb_prime_ctx_create": (_c_i32, [_c_u64, _c_u64, _c_i32, ctypes.POINTER(_c_vp)]),
     "pdb_prime_ctx_destroy": (_c_i32, [_c_vp]),
@@ -211,6 +212,11 @@ def crt_mrc(residues, nprimes: int, n: int, stride: int, primes, limbs, L: int, 
     check(lib.pdb_crt_mrc_u32(ptr(residues), int(nprimes), int(n), int(stride), hp, ptr(limbs), int(L),
                               ptr(neg), ptr(scratch), scratch.numel() * scratch.element_size(),
                               stream_handle(stream)), "crt")
+
+
+def launch_count() -> int:
+    """Kernels this process has launched through the library (all devices)."""
+    return int(load_library().pdb_launch_count())
 
 
 def mulmod_peak(p: int, variant: int) -> float:

@@ -1,0 +1,318 @@
+"""Device parity: every kernel result equals the reference's (golden vectors
+from the reference itself) or the CPU oracle's, bit for bit.  Runs on a B200
+(`pytest -m gpu`)."""
+
+import hashlib
+import random
+
+import numpy as np
+import pytest
+
+from helpers import golden
+import naive
+from oracle import polydet_oracle as O
+from paper_2010_12117_b200 import (
+    CoeffTensor,
+    ModMatrix,
+    ModTensor,
+    PipelineConfig,
+    PolyMatrix,
+    PrimeSpec,
+    TwiddleTable,
+    combine_tensor,
+    condense,
+    det_grid,
+    det_mod,
+    executor,
+    find_fourier_primes,
+    mrc_digits,
+    build_basis,
+    ntt_forward_1d,
+    ntt_forward_multi,
+    ntt_inverse_1d,
+    ntt_inverse_multi,
+    plan,
+    poly_matrix,
+    run,
+    run_report,
+)
+from paper_2010_12117_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+U32 = 2**31
+
+
+def _spec(quad):
+    return PrimeSpec(*quad)
+
+
+def test_ntt_matches_reference_golden(cuda):
+    checked = 0
+    for case in golden("ntt.json"):
+        spec = _spec(case["prime"])
+        if spec.p >= U32:
+            continue
+        shape = tuple(case["shape"])
+        names = tuple("v%d" % i for i in range(len(shape)))
+        t = ModTensor(shape, np.array(case["input"], dtype=np.int64), spec, names)
+        table = TwiddleTable(spec)
+        assert ntt_forward_multi(t, table).residues.tolist() == case["forward"], (spec.p, shape)
+        assert ntt_inverse_multi(t, table).residues.tolist() == case["inverse"], (spec.p, shape)
+        checked += 1
+    assert checked > 50
+
+
+def test_ntt_long_axes_global_path(cuda):
+    spec = find_fourier_primes(16, 1, start=10**9, min_count=1)[0]
+    rng = np.random.default_rng(1)
+    for n in (16384, 65536):
+        x = rng.integers(0, spec.p, n)
+        fwd = ntt_forward_1d(x.tolist(), TwiddleTable(spec))
+        assert fwd.tolist() == O.ntt_multi(x, (n,), spec.p, spec.omega, spec.q).tolist()
+        assert ntt_inverse_1d(fwd.tolist(), TwiddleTable(spec)).tolist() == x.tolist()
+    x = rng.integers(0, spec.p, 2 * 16384)
+    t = ModTensor((2, 16384), x, spec, ("a", "b"))
+    got = ntt_forward_multi(t, TwiddleTable(spec)).residues
+    assert got.tolist() == O.ntt_multi(x, (2, 16384), spec.p, spec.omega, spec.q).tolist()
+
+
+def test_ntt_small_naive_and_errors(cuda):
+    spec = find_fourier_primes(10, 1, start=10**6, min_count=1)[0]
+    table = TwiddleTable(spec)
+    rng = random.Random(2)
+    for n in (1, 2, 4, 8, 32):
+        data = [rng.randrange(spec.p) for _ in range(n)]
+        w = table.root_of_length(n)
+        assert ntt_forward_1d(data, table).tolist() == naive.dft(data, w, spec.p)
+        assert ntt_inverse_1d(data, table).tolist() == naive.idft(data, w, spec.p)
+    with pytest.raises(ValueError, match="unsupported length"):
+        ntt_forward_1d([1, 2, 3], table)
+    with pytest.raises(ValueError, match="unsupported length"):
+        ntt_forward_1d([0] * 2048, table)
+
+
+def test_det_matches_reference_golden(cuda):
+    n = 0
+    for case in golden("det.json"):
+        spec = _spec(case["prime"])
+        if spec.p >= U32:
+            continue
+        grids = [np.array(g, dtype=np.int64) for g in case["grids"]]
+        out = det_grid(grids, case["r"], spec, entry_ids=case["entry_ids"])
+        assert out.tolist() == case["expected"], case["note"]
+        n += 1
+    assert n > 40
+
+
+@pytest.mark.parametrize("r", [4, 9, 16, 17, 33, 40, 64])
+def test_det_random_vs_oracle_with_zero_pivots(cuda, r):
+    spec = find_fourier_primes(8, 1, start=10**9, min_count=1)[0]
+    rng = np.random.default_rng(r)
+    nodes = 700 if r <= 16 else 150
+    mats = rng.integers(0, spec.p, (nodes, r, r))
+    mats[::7, 0, 0] = 0                          # zero leading pivot
+    mats[3::11, r // 2, :] = 0                   # singular
+    mats[5::13, r - 1] = mats[5::13, 0]          # duplicate rows
+    mats[6::17, :, :] = np.triu(mats[6::17, :, :])[:, ::-1, :]  # permuted structure
+    grids = [mats[:, e // r, e % r] for e in range(r * r)]
+    got = det_grid(grids, r, spec)
+    assert got.tolist() == O.det_grid(grids, r, spec.p).tolist()
+
+
+def test_det_dedup_ids_and_31bit_prime(cuda):
+    spec = find_fourier_primes(27, 1, start=2 * 10**9, min_count=1)[0]   # 2013265921 > 2^30
+    rng = np.random.default_rng(3)
+    a, b = rng.integers(0, spec.p, 64), rng.integers(0, spec.p, 64)
+    out = det_grid([a, b], 2, spec, entry_ids=[0, 1, 1, 0])
+    assert out.tolist() == ((a * a - b * b) % spec.p).tolist()
+    for r in (5, 12, 20):
+        mats = rng.integers(0, spec.p, (40, r, r))
+        grids = [mats[:, e // r, e % r] for e in range(r * r)]
+        assert det_grid(grids, r, spec).tolist() == O.det_grid(grids, r, spec.p).tolist()
+
+
+def test_condense_pivot_trail(cuda):
+    spec = find_fourier_primes(4, 1, start=97, min_count=1)[0]
+    rows = [[0, 0, 2], [0, 3, 1], [4, 1, 5]]
+    value, records = condense(ModMatrix.from_rows(rows, spec))
+    assert value == naive.cofactor_det(rows, 97)
+    assert [rec.column for rec in records] == [2, 1, 0]
+    assert sum(rec.flips_sign for rec in records) % 2 == 1
+    value, records = condense(ModMatrix.from_rows([[0, 0], [3, 4]], spec))
+    assert value == 0 and records == []
+    rng = random.Random(4)
+    for _ in range(20):
+        r = rng.randint(1, 6)
+        rows = [[rng.randrange(97) if rng.random() > 0.3 else 0 for _ in range(r)] for _ in range(r)]
+        assert det_mod(ModMatrix.from_rows(rows, spec)) == naive.cofactor_det(rows, 97)
+
+
+def test_crt_matches_reference_golden(cuda):
+    for case in golden("crt.json"):
+        specs = [find_fourier_primes(6, 1, start=p, min_count=1)[0] for p in case["primes"]]
+        n = len(case["residues"][0])
+        tensors = [ModTensor((n,), np.array(r, dtype=np.int64), s, ("x",))
+                   for r, s in zip(case["residues"], specs)]
+        out = combine_tensor(tensors)
+        assert [str(v) for v in out.coeffs] == case["expected"]
+    basis = build_basis([3, 5, 7])
+    assert mrc_digits([2, 3, 2], basis) == [2, 2, 1]
+
+
+def _run_case(case):
+    m = PolyMatrix.from_dict(case["input"])
+    cfg = PipelineConfig(**case["config"])
+    result, _, pl = run_report(m, cfg)
+    assert pl.digest() == case["digest"]
+    assert list(result.shape) == case["shape"]
+    return result.terms(), {tuple(e): c for e, c in case["terms"]}
+
+
+def test_end_to_end_matches_reference_runs(cuda):
+    for case in golden("runs.json"):
+        if case["config"].get("prime_start", 10**9) >= U32:
+            continue
+        got, want = _run_case(case)
+        assert got == want, case["name"]
+
+
+@pytest.mark.parametrize("mode", ["staged", "fused"])
+def test_modes_agree_on_harmonic_rung(cuda, mode, monkeypatch):
+    monkeypatch.setattr(executor, "FORCE_MODE", mode)
+    case = next(c for c in golden("runs.json") if c["name"] == "C4_3src_T5T7_m")
+    got, want = _run_case(case)
+    assert got == want
+
+
+def test_workspace_artifacts_byte_identical_to_reference(cuda, tmp_path):
+    g = golden("workspace.json")
+    m = PolyMatrix.from_dict(g["input"])
+    units = []
+    run(m, PipelineConfig(progress=units.append), workspace=tmp_path / "ws")
+    assert units == g["units"]
+    files = {p.name: hashlib.sha256(p.read_bytes()).hexdigest() for p in (tmp_path / "ws").iterdir()}
+    assert files == g["files"]
+    assert (tmp_path / "ws" / "manifest").read_text().splitlines() == g["manifest"]
+
+
+class _Abort(Exception):
+    pass
+
+
+def _abort_after(n):
+    seen = {"k": 0}
+
+    def hook(unit):
+        seen["k"] += 1
+        if seen["k"] >= n:
+            raise _Abort(unit)
+    return hook
+
+
+def test_kill_and_resume_every_boundary(cuda, tmp_path):
+    from paper_2010_12117_b200 import resume
+
+    rng = random.Random(7)
+    rows = naive.random_poly_matrix(rng, 3, 2, 3, 60, 4, dup=0.3)
+    m = poly_matrix(rows, ("x", "y"))
+    units = []
+    reference = run(m, PipelineConfig(progress=units.append))
+    assert reference.terms() == naive.symbolic_det(rows, 2)
+    pl = plan(m)
+    assert len(units) == pl.prime_count * (m.k + 2) + 1
+    for cut in range(1, len(units)):
+        ws = tmp_path / ("ws%d" % cut)
+        with pytest.raises(_Abort):
+            run(m, PipelineConfig(progress=_abort_after(cut)), workspace=ws)
+        seen = []
+        resumed = resume(ws, PipelineConfig(progress=seen.append))
+        assert resumed.coeffs == reference.coeffs
+        assert len(seen) == len(units) - cut
+    again = []
+    assert run(m, PipelineConfig(progress=again.append), workspace=tmp_path / "ws1").coeffs == reference.coeffs
+    assert again == []
+
+
+def test_edge_cases(cuda):
+    assert run(poly_matrix([[{(1,): 1}]], ("x",))).terms() == {(1,): 1}
+    assert run(poly_matrix([[{}, {}], [{}, {}]], ("x",))).terms() == {}
+    assert run(poly_matrix([[{(0,): 3}, {(0,): 1}], [{(0,): 4}, {(0,): 2}]], ("x",))).terms() == {(0,): 2}
+    m = poly_matrix([[{(): 2}, {(): 1}], [{(): 5}, {(): 7}]], ())
+    out = run(m)
+    assert out.shape == () and out.terms() == {(): 9}
+    m = poly_matrix([[{(1, 0): 1}, {(0, 1): 1}], [{(0, 0): 1}, {(1, 0): 1}]], ("x", "y"))
+    assert run(m).terms() == {(2, 0): 1, (0, 1): -1}
+    a = run(m, PipelineConfig(prime_start=10**9)).coeffs
+    assert run(m, PipelineConfig(prime_start=15 * 10**8)).coeffs == a
+
+
+def test_random_matrices_vs_symbolic(cuda):
+    rng = random.Random(20250808)
+    for _ in range(30):
+        r = rng.randint(1, 5)
+        vn = rng.randint(1, 3)
+        rows = naive.random_poly_matrix(rng, r, vn, rng.randint(0, 3), 100, 4)
+        assert run(poly_matrix(rows, "xyz"[:vn])).terms() == naive.symbolic_det(rows, vn)
+
+
+def test_c3_end_to_end_matches_reference(cuda):
+    g = golden("c3_result.json")
+    m, cfg = workloads.c3()
+    result, timings, pl = run_report(m, cfg)
+    assert pl.digest() == g["digest"]
+    coeffs = result.coeffs
+    for idx, val in g["samples"]:
+        assert coeffs[idx] == int(val)
+    blob = repr((tuple(result.shape), tuple(coeffs), tuple(result.axis_vars))).encode()
+    assert hashlib.sha256(blob).hexdigest() == g["sha256"]
+
+
+@pytest.mark.parametrize("mode", ["fused", "staged"])
+def test_c5_determinants_at_sampled_nodes(cuda, mode):
+    g = golden("c5_det_samples.json")
+    m, cfg = workloads.c5()
+    pl = plan(m, cfg)
+    assert pl.digest() == g["digest"]
+    if mode == "staged" and cuda.cuda.get_device_properties(0).total_memory < 150 << 30:
+        pytest.skip("staged C5 needs ~110 GB")
+    stages = executor.PrimeStages(m, pl, staged=(mode == "staged"))
+    N = pl.shape
+    for sample in g["samples"]:
+        pi = sample["prime_index"]
+        stages.forward(pi)
+        stages.determinants(pi)
+        det = stages.det.cpu().numpy().view(np.uint32)
+        idx = [(a * N[1] + b) * N[2] + c for a, b, c in sample["nodes"]]
+        assert det[idx].tolist() == sample["det"]
+        # size-independent property: interpolation then evaluation is the identity
+        before = stages.det.clone()
+        stages.interpolate(pi)
+        from paper_2010_12117_b200 import native
+        native.ntt_multi(stages.ctx(pi), stages.det, 1, N, None, range(3), False)
+        assert cuda.equal(before, stages.det)
+    del stages
+
+
+def test_schwartz_zippel_full_size_c3(cuda):
+    """Evaluate the final C3 polynomial at a random point mod a fresh prime and
+    compare with the determinant of the entry-wise evaluated matrix."""
+    m, cfg = workloads.c3()
+    out = run(m, cfg)
+    q = 2**61 - 1
+    rng = random.Random(9)
+    point = [rng.randrange(q) for _ in range(3)]
+    lhs = naive.poly_eval(out.terms(), point, q)
+    mat = [[naive.poly_eval(m.entry(i, j).terms(), point, q) for j in range(m.r)] for i in range(m.r)]
+    # Gaussian elimination mod q (q prime)
+    det = 1
+    for c in range(m.r):
+        piv = next(i for i in range(c, m.r) if mat[i][c] % q)
+        if piv != c:
+            mat[c], mat[piv] = mat[piv], mat[c]
+            det = -det
+        det = det * mat[c][c] % q
+        inv = pow(mat[c][c], -1, q)
+        for i in range(c + 1, m.r):
+            f = mat[i][c] * inv % q
+            mat[i] = [(x - f * y) % q for x, y in zip(mat[i], mat[c])]
+    assert lhs == det % q
