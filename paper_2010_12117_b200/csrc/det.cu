@@ -88,36 +88,59 @@ det_small(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t n
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) ids[e] = ids_g[e];
   __syncthreads();
   const uint32_t p = m.p;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < nodes;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t node = node_lo + idx;
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count: every lane takes part in the batched inversion
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < nodes; base += stride) {
+    const int64_t idx = base + lane;
+    const bool valid = idx < nodes;
+    const int64_t node = node_lo + (valid ? idx : 0);
     uint32_t a[R][R];
 #pragma unroll
     for (int i = 0; i < R; ++i)
 #pragma unroll
       for (int j = 0; j < R; ++j) a[i][j] = src.get(ids[i * R + j], node);
-    uint32_t pre = 1 % p, infl = 1 % p;
+    uint32_t preR = m.r1, inflR = m.r1;   // Montgomery forms
     bool ok = true;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const uint32_t z = a[k][k];
       ok = ok && z != 0;
-      pre = mul_mod(pre, z, m);
-      if (k + 1 < R) infl = mul_mod(infl, pre, m);
-      const uint32_t zs = shoup_companion_fast(z, m);
+      const uint32_t zR = to_mont(z, m);
+      preR = mont(preR, zR, m);
+      if (k + 1 < R) inflR = mont(inflR, preR, m);
 #pragma unroll
       for (int i = k + 1; i < R; ++i) {
-        const uint32_t t = a[i][k];
-        const uint32_t ts = shoup_companion_fast(t, m);
+        // row_i <- z*row_i - t*row_k  as one REDC of two 64-bit products
+        const uint32_t tR = to_mont(a[i][k], m);
+        const uint32_t ntR = tR ? p - tR : 0u;
 #pragma unroll
         for (int j = k + 1; j < R; ++j)
-          a[i][j] = sub_mod(shoup_mul(a[i][j], z, zs, p), shoup_mul(a[k][j], t, ts, p), p);
+          a[i][j] = canon32(redc(mad_wide(a[k][j], ntR, mad_wide(a[i][j], zR, 0ull)), m), m);
       }
     }
-    if (ok) {
-      out[idx] = mul_mod(pre, inv_mod(infl, m), m);
-    } else {
-      flag_node(flags, node);
+    // Montgomery batch inversion of the 32 inflations of this warp:
+    // prefix/suffix products by shuffles and a single Fermat exponentiation.
+    const bool use = valid && ok;
+    const uint32_t x = use ? inflR : m.r1;
+    uint32_t pre_x = x, suf_x = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t up = __shfl_up_sync(0xffffffffu, pre_x, d);
+      const uint32_t dn = __shfl_down_sync(0xffffffffu, suf_x, d);
+      if (lane >= d) pre_x = mont(pre_x, up, m);
+      if (lane + d < 32) suf_x = mont(suf_x, dn, m);
+    }
+    const uint32_t totalR = __shfl_sync(0xffffffffu, pre_x, 31);
+    const uint32_t inv_totalR = mont_pow(totalR, (uint64_t)p - 2, m);
+    uint32_t left = __shfl_up_sync(0xffffffffu, pre_x, 1);
+    uint32_t right = __shfl_down_sync(0xffffffffu, suf_x, 1);
+    if (lane == 0) left = m.r1;
+    if (lane == 31) right = m.r1;
+    const uint32_t invR = mont(mont(left, right, m), inv_totalR, m);   // x^-1 * R
+    if (valid) {
+      if (ok) out[idx] = mont(mont(preR, invR, m), 1u, m);
+      else flag_node(flags, node);
     }
   }
 }

@@ -1,30 +1,37 @@
 // det_octet: blocked division-free elimination, 8 lanes per matrix.
 //
-// Why this shape (SURVEY.md §8(d), measured in profiles/intpipe_r01.json):
+// Why this shape (SURVEY.md §8(d); measured in profiles/intpipe_r01.json):
 //   * IMAD.WIDE (64-bit multiply-accumulate) issues at half rate like
 //     IMAD.HI, so a Shoup mul-mod costs 4 fma-heavy slots while a delayed
 //     64-bit MAC costs 2.  Accumulating the B+1 products of a rank-B block
-//     update in 64 bits and reducing once (Montgomery REDC + Barrett) halves
-//     the slot count per elimination update.
+//     update in 64 bits and reducing once (Montgomery REDC + Barrett) cuts the
+//     slot count per elimination update to ~2.7.
 //   * Normalised multipliers need one modular inverse per pivot; with only
-//     ~32 resident 40x40 matrices per SM the per-step Fermat inverses would
-//     cost as much as the updates.  The division-free (condensation) form of
-//     the reference (determinant.py:136-169) needs one inverse per matrix;
-//     here its per-row scalings are folded into scalars (tau, ZP, V below),
-//     so the elimination itself stays at ~(B+1)/B MACs per update.
+//     ~24-32 resident 40x40 matrices per SM those per-step inverses would cost
+//     as much as the updates.  The division-free (condensation) form of the
+//     reference (determinant.py:136-169) needs one inverse per matrix; its
+//     per-row scalings are folded into scalars (tau, ZP, V below).
 //
-// Algorithm for one block of pivots K..K+B-1 (z_s = pivot s, prow_s its row):
-//   row_i after S pivots = ZP[S]*row_i - sum_{s<S} t_s * zeta_s^(S) * prow_s
-//   with ZP[S] = prod_{s<S} z_s, zeta_s^(S) = prod_{s<s'<S} z_s', and the
-//   multipliers t_s = (row_i after s pivots)[K+s], obtained by the recurrence
-//   t_S = ZP[S]*a[i][K+S] + sum_{s<S} t_s * V[s][S],  V[s][S] = -zeta_s^(S) prow_s[K+S].
-//   Pivot rows are stored as NPR = -R*prow mod p (R = 2^32) so that every
-//   accumulation is  a*ZPR + sum tau*NPR  == R*(new value), which a single
-//   REDC turns back into the value.  At most B+1 = 9 products (< 2^60 each
-//   for p < 2^30) are accumulated, inside REDC's bound.
+// One block of pivots K..K+B-1 (z_s = pivot s, prow_s = pivot row s):
+//   P phase (pivot rows, sequential in s): row K+s is final once pivots < s
+//     have been applied; it is stored as NPR_s = -R*prow_s mod p (R = 2^32,
+//     Montgomery form) and applied at once, division-free, to the pending
+//     pivot rows: row_j <- z_s*row_j - row_j[K+s]*prow_s  == REDC(row_j*zR + t*NPR).
+//   T phase (trailing rows, every lane its own rows, no synchronisation):
+//     row_i after the block = ZP[B]*row_i - sum_s tau_s * prow_s with
+//     ZP[S] = prod_{s<S} z_s, tau_s = t_s * prod_{s<s'<B} z_s', and the
+//     multipliers t_s = (row_i after s pivots)[K+s] from the triangular
+//     recurrence t_S = ZP[S]*row_i[K+S] + sum_{s<S} t_s*V[s][S],
+//     V[s][S] = -prow_s[K+S]*prod_{s<s'<S} z_s'.  Each new element is
+//     REDC(row*ZPR + sum tau*NPR): B+1 = 9 MACs, one reduction.
 //   det = prod z_k / prod z_k^(r-1-k) (one inverse per matrix).
 // A zero diagonal pivot aborts the matrix and appends its node to the
-// robust kernel's list.
+// robust kernel's list (first-nonzero pivoting, the reference's rule).
+//
+// Matrix loading (fill): staged grids are gathered with cp.async (no
+// register round trip); fused sources evaluate the last variable in the
+// kernel, 8 nodes at a time with an 8-point NTT when the CTA's matrices are
+// the nodes {o*NL + u + (NL/8) v : v < 8} (fused_dft8), else by Horner.
 #pragma once
 #include "pdb_internal.cuh"
 
@@ -38,6 +45,7 @@ struct OctGeom {
   int S;       // row stride (words), multiple of 4, >= ceil4(r)
   int MS;      // matrix stride (words) incl. scalar area
   int M;       // matrices per CTA iteration (= 4 * warps)
+  int U;       // fused DFT-8 mode: distinct u per iteration (M = 8 U), 0 = off
 };
 
 __host__ __device__ inline int oct_row_stride(int r) {
@@ -46,14 +54,138 @@ __host__ __device__ inline int oct_row_stride(int r) {
   return S;
 }
 
-// scalar area per matrix: V table (B*B), ZPR (B+1), ZETA (B), ZETAs (B), z (B)
-constexpr int OCT_SCALARS = OCT_B * OCT_B + (OCT_B + 1) + 3 * OCT_B;
+// scalar area per matrix: V (B*B), ZPR (B+1), ZETAR (B), ZR (B)
+constexpr int OCT_SCALARS = OCT_B * OCT_B + (OCT_B + 1) + 2 * OCT_B;
 
 __device__ __forceinline__ uint32_t oct_reduce(uint64_t acc, const Mod32& m) {
   return canon32(redc(acc, m), m);
 }
 
-template <class Src>
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// ---- loaders ------------------------------------------------------------------
+// node offset (relative to node_lo) of matrix slot m in iteration it, or -1
+__device__ __forceinline__ int64_t oct_node_linear(int64_t it, int m, const OctGeom& g, int64_t nodes) {
+  int64_t n = it * g.M + m;
+  return n < nodes ? n : -1;
+}
+
+__device__ __forceinline__ int64_t oct_node_dft8(int64_t it, int m, const OctGeom& g, int NL) {
+  const int per_o = NL / (8 * g.U);
+  const int64_t o = it / per_o;
+  const int ublk = (int)(it - o * per_o);
+  const int v = m / g.U, uu = m - v * g.U;
+  return o * NL + ublk * g.U + uu + (int64_t)(NL / 8) * v;
+}
+
+// Position iterator over the r*r real entries without per-element division:
+// flat index pos = first + k*step, tracked as (i, j) with an incremental carry.
+struct PosIter {
+  int i, j, di, dj, r;
+  __device__ __forceinline__ PosIter(int first, int step, int r_) : r(r_) {
+    i = first / r_; j = first - i * r_; di = step / r_; dj = step - di * r_;
+  }
+  __device__ __forceinline__ void next() {
+    i += di; j += dj;
+    if (j >= r) { j -= r; ++i; }
+  }
+};
+
+// Staged grids: thread -> (matrix slot m = t % M, positions t/M + k*(blockDim/M)),
+// gathered with cp.async (consecutive threads read consecutive nodes).
+__device__ __forceinline__ void oct_fill(const StagedSrc& src, uint32_t* mats, const OctGeom& g, const int32_t* ids,
+                         int64_t it, int64_t node_lo, int64_t nodes) {
+  const int r = g.r, S = g.S, M = g.M;
+  const int m = threadIdx.x % M;
+  const int64_t n = oct_node_linear(it, m, g, nodes);
+  if (n >= 0) {
+    const uint32_t* col = src.grids + node_lo + n;
+    uint32_t* dst = mats + (size_t)m * g.MS;
+    PosIter pi(threadIdx.x / M, blockDim.x / M, r);
+    for (; pi.i < r; pi.next())
+      cp_async4(dst + pi.i * S + pi.j, col + (int64_t)ids[pi.i * r + pi.j] * src.stride);
+  }
+  cp_async_wait_all();
+}
+
+// Horner evaluation, any geometry (matrix slot m <-> node it*M + m).
+__device__ __forceinline__ void oct_fill(const FusedSrc& src, uint32_t* mats, const OctGeom& g, const int32_t* ids,
+                         int64_t it, int64_t node_lo, int64_t nodes) {
+  const int r = g.r, S = g.S, M = g.M;
+  const int m = threadIdx.x % M;
+  const int64_t n = oct_node_linear(it, m, g, nodes);
+  if (n < 0) return;
+  uint32_t* dst = mats + (size_t)m * g.MS;
+  PosIter pi(threadIdx.x / M, blockDim.x / M, r);
+  for (; pi.i < r; pi.next()) dst[pi.i * S + pi.j] = src.get(ids[pi.i * r + pi.j], node_lo + n);
+}
+
+// 8 nodes per thread: f(o*NL + u + (NL/8) v) = sum_l Q_l w8^(l v),  Q_l = sum_{l' = l mod 8} T_l' w^(u l').
+__device__ __forceinline__ void oct_fill_dft8(const FusedSrc& src, uint32_t* mats, const OctGeom& g, const int32_t* ids,
+                              int64_t it, int64_t node_lo) {
+  const int r = g.r, S = g.S, U = g.U, NL = src.NL, E = src.E;
+  const uint32_t p = src.p;
+  const int per_o = NL / (8 * U);
+  const int64_t o = (node_lo / NL) + it / per_o;
+  const int ublk = (int)(it % per_o);
+  const int step8 = NL / 8;
+  const uint32_t w1 = __ldg(src.xs + step8), w1s = __ldg(src.xss + step8);
+  const uint32_t w2 = __ldg(src.xs + 2 * step8), w2s = __ldg(src.xss + 2 * step8);
+  const uint32_t w3 = __ldg(src.xs + 3 * step8), w3s = __ldg(src.xss + 3 * step8);
+  const int uu = threadIdx.x % U;
+  // twists w^(u l), l < 8, for this thread's u (indices stepped without any modulo)
+  uint32_t tw[8], tws[8];
+  {
+    const int u = ublk * U + uu;
+    int k = 0;
+#pragma unroll
+    for (int ll = 0; ll < 8; ++ll) {
+      tw[ll] = __ldg(src.xs + k);
+      tws[ll] = __ldg(src.xss + k);
+      k += u;
+      if (k >= NL) k -= NL;
+    }
+  }
+  const size_t ms = (size_t)U * g.MS;
+  uint32_t* slot = mats + (size_t)uu * g.MS;
+  PosIter pi(threadIdx.x / U, blockDim.x / U, r);
+  for (; pi.i < r; pi.next()) {
+    const int i = pi.i, j = pi.j;
+    uint32_t* d = slot + i * S + j;
+    const uint32_t* a = src.part + ((int64_t)ids[i * r + j] * src.outer + o) * E;
+    uint32_t q[8];
+    q[0] = __ldg(a);
+#pragma unroll
+    for (int ll = 1; ll < 8; ++ll)   // E <= 8 on this path (checked at launch)
+      q[ll] = ll < E ? shoup_mul(__ldg(a + ll), tw[ll], tws[ll], p) : 0u;
+    // radix-2 DIT on bit-reversed input -> natural order X[v] = sum_l q_l w8^(l v)
+    uint32_t x0 = q[0], x1 = q[4], x2 = q[2], x3 = q[6], x4 = q[1], x5 = q[5], x6 = q[3], x7 = q[7];
+    uint32_t t;
+    // stage 1 (span 1, twiddle 1)
+    t = x1; x1 = sub_mod(x0, t, p); x0 = add_mod(x0, t, p);
+    t = x3; x3 = sub_mod(x2, t, p); x2 = add_mod(x2, t, p);
+    t = x5; x5 = sub_mod(x4, t, p); x4 = add_mod(x4, t, p);
+    t = x7; x7 = sub_mod(x6, t, p); x6 = add_mod(x6, t, p);
+    // stage 2 (span 2, twiddles 1, w8^2)
+    t = x2; x2 = sub_mod(x0, t, p); x0 = add_mod(x0, t, p);
+    t = shoup_mul(x3, w2, w2s, p); x3 = sub_mod(x1, t, p); x1 = add_mod(x1, t, p);
+    t = x6; x6 = sub_mod(x4, t, p); x4 = add_mod(x4, t, p);
+    t = shoup_mul(x7, w2, w2s, p); x7 = sub_mod(x5, t, p); x5 = add_mod(x5, t, p);
+    // stage 3 (span 4, twiddles 1, w8, w8^2, w8^3)
+    t = x4; x4 = sub_mod(x0, t, p); x0 = add_mod(x0, t, p);
+    t = shoup_mul(x5, w1, w1s, p); x5 = sub_mod(x1, t, p); x1 = add_mod(x1, t, p);
+    t = shoup_mul(x6, w2, w2s, p); x6 = sub_mod(x2, t, p); x2 = add_mod(x2, t, p);
+    t = shoup_mul(x7, w3, w3s, p); x7 = sub_mod(x3, t, p); x3 = add_mod(x3, t, p);
+    d[0] = x0; d[ms] = x1; d[2 * ms] = x2; d[3 * ms] = x3;
+    d[4 * ms] = x4; d[5 * ms] = x5; d[6 * ms] = x6; d[7 * ms] = x7;
+  }
+}
+
+template <class Src, bool DFT8>
 __global__ void __launch_bounds__(256)
 det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t nodes,
                  uint32_t* __restrict__ out, unsigned long long* __restrict__ flag_count,
@@ -67,122 +199,111 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
   const unsigned omask = 0xffu << (oct * 8);
   const int my = warp * 4 + oct;                       // matrix slot within the CTA
   uint32_t* A = mats + (size_t)my * g.MS;
-  uint32_t* V = A + r * S;                             // [B][B]
-  uint32_t* ZPR = V + OCT_B * OCT_B;                   // [B+1]
-  uint32_t* ZETA = ZPR + OCT_B + 1;                    // [B]
-  uint32_t* ZETAs = ZETA + OCT_B;                      // [B]
-  uint32_t* Z = ZETAs + OCT_B;                         // [B] raw pivots of this block
+  uint32_t* V = A + r * S;                             // [B][B]  V[s][S] (R-scaled, negated)
+  uint32_t* ZPR = V + OCT_B * OCT_B;                   // [B+1]   prod_{s<S} z_s * R
+  uint32_t* ZETAR = ZPR + OCT_B + 1;                   // [B]     prod_{s<s'<B} z_s' * R
+  uint32_t* ZR = ZETAR + OCT_B;                        // [B]     z_s * R
   const uint32_t p = m.p;
-  const int nwarps = blockDim.x >> 5;
+  const int cend = (r + 3) & ~3;
 
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) ids[e] = ids_g[e];
+  // padding columns [r, S) are zeroed once: fills write only the r*r real
+  // entries and the elimination keeps padding at zero (0*ZPR + sum tau*0)
+  for (int w = threadIdx.x; w < g.M * g.MS; w += blockDim.x) mats[w] = 0;
+  const int64_t iters = (nodes + g.M - 1) / g.M;
 
-  for (int64_t base = (int64_t)blockIdx.x * g.M; base < nodes; base += (int64_t)gridDim.x * g.M) {
+  for (int64_t it = blockIdx.x; it < iters; it += gridDim.x) {
     __syncthreads();
-    // ---- load: warp w fills positions w, w+nw, ...; lane = matrix slot ----
-    const int nload = (int)((nodes - base) < g.M ? (nodes - base) : g.M);
-    for (int pos = warp; pos < r * S; pos += nwarps) {
-      const int i = pos / S, j = pos - i * S;
-      if (lane < g.M) {
-        uint32_t v = 0;
-        if (j < r && lane < nload) v = src.get(ids[i * r + j], node_lo + base + lane);
-        mats[(size_t)lane * g.MS + pos] = v;
-      }
-    }
+    if constexpr (DFT8) oct_fill_dft8(src, mats, g, ids, it, node_lo);
+    else oct_fill(src, mats, g, ids, it, node_lo, nodes);
     __syncthreads();
-    if (my >= nload) continue;
-    const int64_t node = node_lo + base + my;
+    int64_t node;
+    if constexpr (DFT8) node = oct_node_dft8(it, my, g, src.NL);
+    else node = oct_node_linear(it, my, g, nodes);
+    if (node < 0) continue;
 
-    uint32_t pre = 1, infl = 1;
+    uint32_t preR = m.r1, inflR = m.r1;   // Montgomery forms of prod z and prod z^(r-1-k)
     bool ok = true;
     for (int K = 0; K < r && ok; K += OCT_B) {
       const int Bk = (r - K) < OCT_B ? (r - K) : OCT_B;
-      if (l == 0) ZPR[0] = m.r1;
-      __syncwarp(omask);
-      // ---------------- pivot rows ----------------
+      // ---------------- P phase: pivot rows ----------------
       for (int s = 0; s < Bk; ++s) {
         const int k = K + s;
-        // multipliers t_0..t_{s-1} of row k (every lane, redundantly)
-        uint32_t t[OCT_B], tau[OCT_B];
-#pragma unroll
-        for (int q = 0; q < OCT_B; ++q) {
-          if (q < s) {
-            uint64_t acc = (uint64_t)A[k * S + K + q] * ZPR[q];
-#pragma unroll
-            for (int s2 = 0; s2 < OCT_B; ++s2)
-              if (s2 < q) acc += (uint64_t)t[s2] * V[s2 * OCT_B + q];
-            t[q] = oct_reduce(acc, m);
-          }
-        }
-        // tau_q = t_q * prod_{q<s'<s} z_s'
-        uint32_t zeta = 1;
-#pragma unroll
-        for (int q = OCT_B - 1; q >= 0; --q) {
-          if (q < s) {
-            tau[q] = mul_mod(t[q], zeta, m);
-            zeta = mul_mod(zeta, Z[q], m);
-          }
-        }
-        const uint32_t zpr = ZPR[s];
-        for (int c = k + l; c < r; c += OCT_LPM) {
-          uint64_t acc = (uint64_t)A[k * S + c] * zpr;
-#pragma unroll
-          for (int q = 0; q < OCT_B; ++q)
-            if (q < s) acc += (uint64_t)tau[q] * A[(K + q) * S + c];
-          const uint32_t v = oct_reduce(acc, m);
-          if (c == k) {
-            A[k * S + c] = v;
-          } else {
-            const uint32_t vr = shoup_mul(v, m.r1, m.r1s, p);
-            A[k * S + c] = vr ? p - vr : 0u;     // NPR_s[c] = -R * prow_s[c]
-          }
-        }
-        __syncwarp(omask);
         const uint32_t z = A[k * S + k];
         if (z == 0) { ok = false; break; }
-        pre = mul_mod(pre, z, m);
-        if (k + 1 < r) infl = mul_mod(infl, pre, m);
-        if (l == 0) {
-          Z[s] = z;
-          ZPR[s + 1] = mul_mod(ZPR[s], z, m);
+        const uint32_t zR = to_mont(z, m);
+        preR = mont(preR, zR, m);
+        if (k + 1 < r) inflR = mont(inflR, preR, m);
+        if (l == 0) ZR[s] = zR;
+        // row k is final: store NPR_s[c] = -R * prow_s[c] for c > k
+        uint32_t* prow = A + k * S;
+        for (int c = k + 1 + l; c < r; c += OCT_LPM) {
+          const uint32_t vr = to_mont(prow[c], m);
+          prow[c] = vr ? p - vr : 0u;
         }
-        // V[q][s+1] = NPR_q[K+s+1] * prod_{q<s'<=s} z_s'  (column s+1 of the table)
-        if (s + 1 < Bk && l <= s) {
-          uint32_t prod = 1;
-          for (int s2 = l + 1; s2 < s; ++s2) prod = mul_mod(prod, A[(K + s2) * S + K + s2], m);
-          if (l < s) prod = mul_mod(prod, z, m);
-          V[l * OCT_B + s + 1] = mul_mod(A[(K + l) * S + K + s + 1], prod, m);
+        __syncwarp(omask);
+        // pending pivot rows j in (k, K+Bk): rank-1 division-free update, the
+        // (j, c) items flattened over the 8 lanes (incremental index, no division)
+        const int nc = r - k - 1;
+        const int items = (K + Bk - k - 1) * nc;
+        if (items > 0) {
+          const int dj = OCT_LPM / nc, dc = OCT_LPM - dj * nc;
+          int jj = l / nc, cc = l - jj * nc;
+          for (int idx = l; idx < items; idx += OCT_LPM) {
+            uint32_t* rj = A + (k + 1 + jj) * S;
+            const int c = k + 1 + cc;
+            rj[c] = oct_reduce(mad_wide(rj[k], prow[c], mad_wide(rj[c], zR, 0ull)), m);
+            jj += dj;
+            cc += dc;
+            if (cc >= nc) { cc -= nc; ++jj; }
+          }
         }
         __syncwarp(omask);
       }
       if (!ok) break;
-      // zeta_q = prod_{q<s'<Bk} z_s'  (Shoup constants for the trailing rows)
-      if (l == 0) {
-        uint32_t zeta = 1;
-        for (int q = Bk - 1; q >= 0; --q) {
-          ZETA[q] = zeta;
-          ZETAs[q] = shoup_companion_fast(zeta, m);
-          zeta = mul_mod(zeta, Z[q], m);
+      if (K + OCT_B >= r) break;       // no trailing rows: elimination done
+      // ---------------- block scalars (lane q <-> pivot q) ----------------
+      {
+        const int q = l;
+        uint32_t zz = m.r1;            // prod_{q<s'<s} z_s' * R
+        for (int s = q + 1; s < OCT_B; ++s) {
+          V[q * OCT_B + s] = mont(A[(K + q) * S + K + s], zz, m);
+          zz = mont(zz, ZR[s], m);
+        }
+        ZETAR[q] = zz;
+        if (l == 0) {
+          uint32_t zp = m.r1;
+          ZPR[0] = zp;
+          for (int s = 0; s < OCT_B; ++s) { zp = mont(zp, ZR[s], m); ZPR[s + 1] = zp; }
         }
       }
       __syncwarp(omask);
-      // ---------------- trailing rows (lanes split rows) ----------------
-      // Trailing rows exist only when r - K > B, i.e. for full blocks (Bk == OCT_B),
-      // so everything below is unrolled over the compile-time block size.
+      // ---------------- T phase: trailing rows (lanes split rows) ----------------
       const int c0 = K + OCT_B;
-      const int cend = (r + 3) & ~3;
       const uint32_t zpr = ZPR[OCT_B];
       const uint32_t* npr = A + K * S;                  // NPR_q[c] = npr[q * S + c]
+      // block scalars in registers (shared by all of this lane's rows)
+      uint32_t vr[OCT_B * (OCT_B - 1) / 2], zp[OCT_B], ze[OCT_B];
+#pragma unroll
+      for (int q = 0; q < OCT_B; ++q) {
+        zp[q] = ZPR[q];
+        ze[q] = ZETAR[q];
+#pragma unroll
+        for (int s2 = 0; s2 < q; ++s2) vr[q * (q - 1) / 2 + s2] = V[s2 * OCT_B + q];
+      }
       for (int i = c0 + l; i < r; i += OCT_LPM) {
         uint32_t* row = A + i * S;
         uint32_t t[OCT_B], tau[OCT_B];
+        const uint4 pa = *reinterpret_cast<const uint4*>(row + K);      // panel of row i
+        const uint4 pb = *reinterpret_cast<const uint4*>(row + K + 4);
+        const uint32_t pan[OCT_B] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
 #pragma unroll
         for (int q = 0; q < OCT_B; ++q) {
-          uint64_t acc = mad_wide(row[K + q], ZPR[q], 0ull);
+          uint64_t acc = mad_wide(pan[q], zp[q], 0ull);
 #pragma unroll
-          for (int s2 = 0; s2 < q; ++s2) acc = mad_wide(t[s2], V[s2 * OCT_B + q], acc);
+          for (int s2 = 0; s2 < q; ++s2) acc = mad_wide(t[s2], vr[q * (q - 1) / 2 + s2], acc);
           t[q] = oct_reduce(acc, m);
-          tau[q] = shoup_mul(t[q], ZETA[q], ZETAs[q], p);
+          tau[q] = mont(t[q], ze[q], m);
         }
         for (int c = c0; c < cend; c += 4) {
           const uint4 a4 = *reinterpret_cast<const uint4*>(row + c);
@@ -208,21 +329,25 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
     }
     if (l == 0) {
       if (ok) {
-        out[node - node_lo] = mul_mod(pre, inv_mod(infl, m), m);
+        // det = prod z / prod z^(r-1-k); Fermat inverse in Montgomery form:
+        // mont_pow(infl*R, p-2) = infl^-1 * R, mont(pre*R, .) = det*R, mont(., 1) = det
+        const uint32_t invR = mont_pow(inflR, (uint64_t)p - 2, m);
+        out[node] = mont(mont(preR, invR, m), 1u, m);
       } else {
         unsigned long long slot = atomicAdd(flag_count, 1ull);
-        flag_nodes[slot] = node;
+        flag_nodes[slot] = node_lo + node;
       }
     }
   }
 }
 
-inline OctGeom oct_geom(int r, int warps) {
+inline OctGeom oct_geom(int r, int warps, int U) {
   OctGeom g;
   g.r = r;
   g.S = oct_row_stride(r);
   g.MS = ((r * g.S + OCT_SCALARS + 3) & ~3);
   g.M = 4 * warps;
+  g.U = U;
   return g;
 }
 
@@ -230,26 +355,58 @@ inline size_t oct_smem(const OctGeom& g) {
   return sizeof(uint32_t) * ((size_t)((g.r * g.r + 3) & ~3) + (size_t)g.M * g.MS);
 }
 
-template <class Src>
-int launch_octet(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int64_t node_lo, int64_t nodes,
-                 uint32_t* out, unsigned long long* flag_count, int64_t* flag_nodes, cudaStream_t st) {
-  // largest CTA (<= 8 warps) such that two CTAs fit on an SM
-  int warps = 8;
-  OctGeom g = oct_geom(r, warps);
-  while (warps > 1 && oct_smem(g) > 112 * 1024) g = oct_geom(r, --warps);
+// Choose warps per CTA so that several CTAs share an SM (load/compute overlap).
+inline OctGeom oct_pick(int r, int64_t nodes, bool dft8) {
+  const size_t budget = 224 * 1024;
+  OctGeom best = oct_geom(r, 2, dft8 ? 1 : 0);
+  double best_score = -1;
+  for (int warps = 2; warps <= 8; warps += 2) {
+    OctGeom g = oct_geom(r, warps, dft8 ? warps / 2 : 0);
+    const size_t sm = oct_smem(g) + 1024;
+    const int ctas = (int)(budget / sm);
+    if (ctas < 1) continue;
+    const int resident = ctas * warps > 32 ? 32 : ctas * warps;   // warps per SM
+    const double score = resident + 0.01 * ctas;   // ties: more CTAs overlap fill and elimination
+    if (score > best_score) { best_score = score; best = g; }
+  }
+  return best;
+}
+
+template <class Src, bool DFT8>
+int launch_octet_geom(PrimeCtx* ctx, const OctGeom& g, Src src, const int32_t* ids, int64_t node_lo,
+                      int64_t nodes, uint32_t* out, unsigned long long* flag_count, int64_t* flag_nodes,
+                      cudaStream_t st) {
   const size_t smem = oct_smem(g);
-  static bool attr_set[2] = {false, false};
-  (void)attr_set;
-  if (cudaFuncSetAttribute(det_octet_kernel<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(det_octet_kernel<Src, DFT8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return check_launch("det_octet attribute");
-  int64_t ctas = (nodes + g.M - 1) / g.M;
-  int64_t cap = (int64_t)ctx->sms * 2;
-  int grid = (int)(ctas < cap ? ctas : cap);
-  det_octet_kernel<Src><<<grid, warps * 32, smem, st>>>(src, ids, node_lo, nodes, out, flag_count,
-                                                        flag_nodes, g, ctx->m);
+  const int ctas_per_sm = (int)((224 * 1024) / (smem + 1024));
+  const int64_t iters = (nodes + g.M - 1) / g.M;
+  const int64_t cap = (int64_t)ctx->sms * (ctas_per_sm > 0 ? ctas_per_sm : 1);
+  const int grid = (int)(iters < cap ? iters : cap);
+  det_octet_kernel<Src, DFT8><<<grid, g.M * 8, smem, st>>>(src, ids, node_lo, nodes, out, flag_count,
+                                                            flag_nodes, g, ctx->m);
   count_launch();
   return check_launch("det_octet");
+}
+
+inline int launch_octet(PrimeCtx* ctx, int r, StagedSrc src, const int32_t* ids, int64_t node_lo,
+                        int64_t nodes, uint32_t* out, unsigned long long* flag_count, int64_t* flag_nodes,
+                        cudaStream_t st) {
+  const OctGeom g = oct_pick(r, nodes, false);
+  return launch_octet_geom<StagedSrc, false>(ctx, g, src, ids, node_lo, nodes, out, flag_count, flag_nodes, st);
+}
+
+inline int launch_octet(PrimeCtx* ctx, int r, FusedSrc src, const int32_t* ids, int64_t node_lo,
+                        int64_t nodes, uint32_t* out, unsigned long long* flag_count, int64_t* flag_nodes,
+                        cudaStream_t st) {
+  OctGeom g = oct_pick(r, nodes, true);
+  const bool dft8 = src.E <= 8 && src.NL >= 8 && src.NL % (8 * g.U) == 0 && node_lo % src.NL == 0 &&
+                    nodes % src.NL == 0;
+  if (dft8)
+    return launch_octet_geom<FusedSrc, true>(ctx, g, src, ids, node_lo, nodes, out, flag_count, flag_nodes, st);
+  g = oct_pick(r, nodes, false);
+  return launch_octet_geom<FusedSrc, false>(ctx, g, src, ids, node_lo, nodes, out, flag_count, flag_nodes, st);
 }
 
 }  // namespace pdb

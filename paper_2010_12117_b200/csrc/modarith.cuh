@@ -110,6 +110,26 @@ PDB_HD uint32_t canon32(uint32_t v, const Mod32& m) {
   return csub(v - q * m.p, m.p);
 }
 
+// Montgomery product a * b * 2^-32 mod p, canonical (a, b < 2^32, a*b < (2^32-p-1) 2^32).
+// With b = x*R mod p ("Montgomery form") this is the plain product a*x.
+PDB_HD uint32_t mont(uint32_t a, uint32_t b, const Mod32& m) {
+  return canon32(redc(mad_wide(a, b, 0ull), m), m);
+}
+
+// x -> x*R mod p (R = 2^32), canonical.
+PDB_HD uint32_t to_mont(uint32_t x, const Mod32& m) { return shoup_mul(x, m.r1, m.r1s, m.p); }
+
+// (a*R)^e * R mod p for aR in Montgomery form (square and multiply).
+PDB_HD uint32_t mont_pow(uint32_t aR, uint64_t e, const Mod32& m) {
+  uint32_t r = m.r1, b = aR;
+  while (e) {
+    if (e & 1) r = mont(r, b, m);
+    b = mont(b, b, m);
+    e >>= 1;
+  }
+  return r;
+}
+
 PDB_HD uint32_t pow_mod(uint32_t a, uint64_t e, const Mod32& m) {
   uint32_t r = 1 % m.p, b = a;
   while (e) {
