@@ -33,6 +33,7 @@
 // kernel, 8 nodes at a time with an 8-point NTT when the CTA's matrices are
 // the nodes {o*NL + u + (NL/8) v : v < 8} (fused_dft8), else by Horner.
 #pragma once
+#include <cstdlib>
 #include "pdb_internal.cuh"
 
 namespace pdb {
@@ -185,19 +186,22 @@ __device__ __forceinline__ void oct_fill_dft8(const FusedSrc& src, uint32_t* mat
   }
 }
 
-template <class Src, bool DFT8>
+template <class Src, bool DFT8, int LPM>
 __global__ void __launch_bounds__(256)
 det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t nodes,
                  uint32_t* __restrict__ out, unsigned long long* __restrict__ flag_count,
                  int64_t* __restrict__ flag_nodes, OctGeom g, Mod32 m) {
+  static_assert(LPM == 8 || LPM == 16, "8 or 16 lanes per matrix");
+  constexpr int GPW = 32 / LPM;                        // matrices per warp
+  constexpr int HALVES = LPM / 8;                      // lanes sharing a trailing row
   extern __shared__ __align__(16) uint32_t smem[];
   const int r = g.r, S = g.S;
   int32_t* ids = reinterpret_cast<int32_t*>(smem);                  // r*r ids
   uint32_t* mats = smem + ((r * r + 3) & ~3);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int oct = lane >> 3, l = lane & 7;
-  const unsigned omask = 0xffu << (oct * 8);
-  const int my = warp * 4 + oct;                       // matrix slot within the CTA
+  const int grp = lane / LPM, l = lane % LPM;
+  const unsigned omask = (LPM == 32 ? 0xffffffffu : ((1u << LPM) - 1u)) << (grp * LPM);
+  const int my = warp * GPW + grp;                     // matrix slot within the CTA
   uint32_t* A = mats + (size_t)my * g.MS;
   uint32_t* V = A + r * S;                             // [B][B]  V[s][S] (R-scaled, negated)
   uint32_t* ZPR = V + OCT_B * OCT_B;                   // [B+1]   prod_{s<S} z_s * R
@@ -235,27 +239,47 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
         preR = mont(preR, zR, m);
         if (k + 1 < r) inflR = mont(inflR, preR, m);
         if (l == 0) ZR[s] = zR;
-        // row k is final: store NPR_s[c] = -R * prow_s[c] for c > k
+        // 4-column chunks from a0 (<= k+1); columns <= k keep their value
+        const int a0 = (k + 1) & ~3;
+        const int nch = (cend - a0) >> 2;
         uint32_t* prow = A + k * S;
-        for (int c = k + 1 + l; c < r; c += OCT_LPM) {
-          const uint32_t vr = to_mont(prow[c], m);
-          prow[c] = vr ? p - vr : 0u;
+        // row k is final: NPR_s[c] = -R * prow_s[c] for c > k
+        for (int ch = l; ch < nch; ch += LPM) {
+          const int c = a0 + 4 * ch;
+          uint4 v = *reinterpret_cast<const uint4*>(prow + c);
+          uint32_t t0 = to_mont(v.x, m), t1 = to_mont(v.y, m), t2 = to_mont(v.z, m), t3 = to_mont(v.w, m);
+          t0 = t0 ? p - t0 : 0u; t1 = t1 ? p - t1 : 0u; t2 = t2 ? p - t2 : 0u; t3 = t3 ? p - t3 : 0u;
+          if (c + 0 > k) v.x = t0;
+          if (c + 1 > k) v.y = t1;
+          if (c + 2 > k) v.z = t2;
+          if (c + 3 > k) v.w = t3;
+          *reinterpret_cast<uint4*>(prow + c) = v;
         }
         __syncwarp(omask);
-        // pending pivot rows j in (k, K+Bk): rank-1 division-free update, the
-        // (j, c) items flattened over the 8 lanes (incremental index, no division)
-        const int nc = r - k - 1;
-        const int items = (K + Bk - k - 1) * nc;
+        // pending pivot rows j in (k, K+Bk): rank-1 division-free update
+        //   row_j <- z*row_j - row_j[k]*prow  ==  REDC(row_j*zR + row_j[k]*NPR)
+        const int items = (K + Bk - k - 1) * nch;
         if (items > 0) {
-          const int dj = OCT_LPM / nc, dc = OCT_LPM - dj * nc;
-          int jj = l / nc, cc = l - jj * nc;
-          for (int idx = l; idx < items; idx += OCT_LPM) {
+          const int dj = LPM / nch, dc = LPM - dj * nch;
+          int jj = l / nch, cc = l - jj * nch;
+          for (int idx = l; idx < items; idx += LPM) {
             uint32_t* rj = A + (k + 1 + jj) * S;
-            const int c = k + 1 + cc;
-            rj[c] = oct_reduce(mad_wide(rj[k], prow[c], mad_wide(rj[c], zR, 0ull)), m);
+            const int c = a0 + 4 * cc;
+            const uint32_t tj = rj[k];
+            const uint4 np = *reinterpret_cast<const uint4*>(prow + c);
+            uint4 a = *reinterpret_cast<const uint4*>(rj + c);
+            const uint32_t n0 = oct_reduce(mad_wide(tj, np.x, mad_wide(a.x, zR, 0ull)), m);
+            const uint32_t n1 = oct_reduce(mad_wide(tj, np.y, mad_wide(a.y, zR, 0ull)), m);
+            const uint32_t n2 = oct_reduce(mad_wide(tj, np.z, mad_wide(a.z, zR, 0ull)), m);
+            const uint32_t n3 = oct_reduce(mad_wide(tj, np.w, mad_wide(a.w, zR, 0ull)), m);
+            if (c + 0 > k) a.x = n0;
+            if (c + 1 > k) a.y = n1;
+            if (c + 2 > k) a.z = n2;
+            if (c + 3 > k) a.w = n3;
+            *reinterpret_cast<uint4*>(rj + c) = a;
             jj += dj;
             cc += dc;
-            if (cc >= nc) { cc -= nc; ++jj; }
+            if (cc >= nch) { cc -= nch; ++jj; }
           }
         }
         __syncwarp(omask);
@@ -263,7 +287,7 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
       if (!ok) break;
       if (K + OCT_B >= r) break;       // no trailing rows: elimination done
       // ---------------- block scalars (lane q <-> pivot q) ----------------
-      {
+      if (l < OCT_B) {
         const int q = l;
         uint32_t zz = m.r1;            // prod_{q<s'<s} z_s' * R
         for (int s = q + 1; s < OCT_B; ++s) {
@@ -278,11 +302,11 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
         }
       }
       __syncwarp(omask);
-      // ---------------- T phase: trailing rows (lanes split rows) ----------------
+      // ---------------- T phase: trailing rows ----------------
+      // lane l: rows c0 + (l % 8) + 8u, column chunks (l / 8) + HALVES*v
       const int c0 = K + OCT_B;
       const uint32_t zpr = ZPR[OCT_B];
       const uint32_t* npr = A + K * S;                  // NPR_q[c] = npr[q * S + c]
-      // block scalars in registers (shared by all of this lane's rows)
       uint32_t vr[OCT_B * (OCT_B - 1) / 2], zp[OCT_B], ze[OCT_B];
 #pragma unroll
       for (int q = 0; q < OCT_B; ++q) {
@@ -291,7 +315,8 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
 #pragma unroll
         for (int s2 = 0; s2 < q; ++s2) vr[q * (q - 1) / 2 + s2] = V[s2 * OCT_B + q];
       }
-      for (int i = c0 + l; i < r; i += OCT_LPM) {
+      const int half = l >> 3;
+      for (int i = c0 + (l & 7); i < r; i += 8) {
         uint32_t* row = A + i * S;
         uint32_t t[OCT_B], tau[OCT_B];
         const uint4 pa = *reinterpret_cast<const uint4*>(row + K);      // panel of row i
@@ -305,7 +330,7 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
           t[q] = oct_reduce(acc, m);
           tau[q] = mont(t[q], ze[q], m);
         }
-        for (int c = c0; c < cend; c += 4) {
+        for (int c = c0 + 4 * half; c < cend; c += 4 * HALVES) {
           const uint4 a4 = *reinterpret_cast<const uint4*>(row + c);
           uint64_t a0 = mad_wide(a4.x, zpr, 0ull), a1 = mad_wide(a4.y, zpr, 0ull);
           uint64_t a2 = mad_wide(a4.z, zpr, 0ull), a3 = mad_wide(a4.w, zpr, 0ull);
@@ -341,13 +366,13 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
   }
 }
 
-inline OctGeom oct_geom(int r, int warps, int U) {
+inline OctGeom oct_geom(int r, int warps, int lpm, bool dft8) {
   OctGeom g;
   g.r = r;
   g.S = oct_row_stride(r);
   g.MS = ((r * g.S + OCT_SCALARS + 3) & ~3);
-  g.M = 4 * warps;
-  g.U = U;
+  g.M = warps * (32 / lpm);
+  g.U = dft8 ? g.M / 8 : 0;
   return g;
 }
 
@@ -355,58 +380,74 @@ inline size_t oct_smem(const OctGeom& g) {
   return sizeof(uint32_t) * ((size_t)((g.r * g.r + 3) & ~3) + (size_t)g.M * g.MS);
 }
 
-// Choose warps per CTA so that several CTAs share an SM (load/compute overlap).
-inline OctGeom oct_pick(int r, int64_t nodes, bool dft8) {
+// Choose warps per CTA so that several CTAs share an SM (load/compute overlap)
+// and the resident warp count is largest.
+inline OctGeom oct_pick(int r, int lpm, bool dft8) {
   const size_t budget = 224 * 1024;
-  OctGeom best = oct_geom(r, 2, dft8 ? 1 : 0);
+  OctGeom best = oct_geom(r, 32 / (32 / lpm) / 4 * 2, lpm, dft8);
   double best_score = -1;
-  for (int warps = 2; warps <= 8; warps += 2) {
-    OctGeom g = oct_geom(r, warps, dft8 ? warps / 2 : 0);
+  for (int warps = 1; warps <= 8; ++warps) {
+    OctGeom g = oct_geom(r, warps, lpm, dft8);
+    if (dft8 && (g.M % 8)) continue;
     const size_t sm = oct_smem(g) + 1024;
     const int ctas = (int)(budget / sm);
     if (ctas < 1) continue;
-    const int resident = ctas * warps > 32 ? 32 : ctas * warps;   // warps per SM
-    const double score = resident + 0.01 * ctas;   // ties: more CTAs overlap fill and elimination
+    const int resident = ctas * warps > 48 ? 48 : ctas * warps;   // warps per SM
+    const double score = resident + 0.01 * ctas;
     if (score > best_score) { best_score = score; best = g; }
   }
   return best;
 }
 
-template <class Src, bool DFT8>
+template <class Src, bool DFT8, int LPM>
 int launch_octet_geom(PrimeCtx* ctx, const OctGeom& g, Src src, const int32_t* ids, int64_t node_lo,
                       int64_t nodes, uint32_t* out, unsigned long long* flag_count, int64_t* flag_nodes,
                       cudaStream_t st) {
   const size_t smem = oct_smem(g);
-  if (cudaFuncSetAttribute(det_octet_kernel<Src, DFT8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(det_octet_kernel<Src, DFT8, LPM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return check_launch("det_octet attribute");
   const int ctas_per_sm = (int)((224 * 1024) / (smem + 1024));
   const int64_t iters = (nodes + g.M - 1) / g.M;
   const int64_t cap = (int64_t)ctx->sms * (ctas_per_sm > 0 ? ctas_per_sm : 1);
   const int grid = (int)(iters < cap ? iters : cap);
-  det_octet_kernel<Src, DFT8><<<grid, g.M * 8, smem, st>>>(src, ids, node_lo, nodes, out, flag_count,
-                                                            flag_nodes, g, ctx->m);
+  const int threads = g.M * LPM;
+  det_octet_kernel<Src, DFT8, LPM><<<grid, threads, smem, st>>>(src, ids, node_lo, nodes, out, flag_count,
+                                                                 flag_nodes, g, ctx->m);
   count_launch();
   return check_launch("det_octet");
+}
+
+// lanes per matrix: 16 for the larger orders (more resident warps per SM), 8 below
+inline int oct_lpm(int r) {
+  static const char* env = getenv("PDB_OCT_LPM");
+  if (env) return atoi(env) == 16 ? 16 : 8;
+  return r >= 24 ? 16 : 8;
+}
+
+template <class Src, bool DFT8>
+int launch_octet_lpm(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int64_t node_lo, int64_t nodes,
+                     uint32_t* out, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
+  if (oct_lpm(r) == 16)
+    return launch_octet_geom<Src, DFT8, 16>(ctx, oct_pick(r, 16, DFT8), src, ids, node_lo, nodes, out, fc, fn, st);
+  return launch_octet_geom<Src, DFT8, 8>(ctx, oct_pick(r, 8, DFT8), src, ids, node_lo, nodes, out, fc, fn, st);
 }
 
 inline int launch_octet(PrimeCtx* ctx, int r, StagedSrc src, const int32_t* ids, int64_t node_lo,
                         int64_t nodes, uint32_t* out, unsigned long long* flag_count, int64_t* flag_nodes,
                         cudaStream_t st) {
-  const OctGeom g = oct_pick(r, nodes, false);
-  return launch_octet_geom<StagedSrc, false>(ctx, g, src, ids, node_lo, nodes, out, flag_count, flag_nodes, st);
+  return launch_octet_lpm<StagedSrc, false>(ctx, r, src, ids, node_lo, nodes, out, flag_count, flag_nodes, st);
 }
 
 inline int launch_octet(PrimeCtx* ctx, int r, FusedSrc src, const int32_t* ids, int64_t node_lo,
                         int64_t nodes, uint32_t* out, unsigned long long* flag_count, int64_t* flag_nodes,
                         cudaStream_t st) {
-  OctGeom g = oct_pick(r, nodes, true);
+  const OctGeom g = oct_pick(r, oct_lpm(r), true);
   const bool dft8 = src.E <= 8 && src.NL >= 8 && src.NL % (8 * g.U) == 0 && node_lo % src.NL == 0 &&
                     nodes % src.NL == 0;
   if (dft8)
-    return launch_octet_geom<FusedSrc, true>(ctx, g, src, ids, node_lo, nodes, out, flag_count, flag_nodes, st);
-  g = oct_pick(r, nodes, false);
-  return launch_octet_geom<FusedSrc, false>(ctx, g, src, ids, node_lo, nodes, out, flag_count, flag_nodes, st);
+    return launch_octet_lpm<FusedSrc, true>(ctx, r, src, ids, node_lo, nodes, out, flag_count, flag_nodes, st);
+  return launch_octet_lpm<FusedSrc, false>(ctx, r, src, ids, node_lo, nodes, out, flag_count, flag_nodes, st);
 }
 
 }  // namespace pdb
