@@ -56,7 +56,8 @@ __host__ __device__ inline int oct_row_stride(int r) {
 }
 
 // scalar area per matrix: V (B*B), ZPR (B+1), ZETAR (B), ZR (B)
-constexpr int OCT_SCALARS = OCT_B * OCT_B + (OCT_B + 1) + 2 * OCT_B;
+constexpr int PBW = 2 * OCT_B;   // P-panel row width
+constexpr int OCT_SCALARS = OCT_B * PBW + OCT_B * OCT_B + (OCT_B + 1) + 2 * OCT_B + 3;
 
 __device__ __forceinline__ uint32_t oct_reduce(uint64_t acc, const Mod32& m) {
   return canon32(redc(acc, m), m);
@@ -186,6 +187,25 @@ __device__ __forceinline__ void oct_fill_dft8(const FusedSrc& src, uint32_t* mat
   }
 }
 
+// Multipliers of one trailing row w.r.t. the block's pivots:
+// t_q = ZP[q]*pan[q] - sum_{s<q} t_s prow_s[K+q] prod_{s<s'<q} z_s'  (REDC of R-scaled
+// constants), tau_q = t_q * prod_{q<s'<B} z_s'.
+__device__ __forceinline__ void oct_chain(const uint32_t* pan_ptr, const uint32_t* zp, const uint32_t* vr,
+                                          const uint32_t* ze, const Mod32& m, uint32_t* tau) {
+  const uint4 pa = *reinterpret_cast<const uint4*>(pan_ptr);
+  const uint4 pb = *reinterpret_cast<const uint4*>(pan_ptr + 4);
+  const uint32_t pan[OCT_B] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+  uint32_t t[OCT_B];
+#pragma unroll
+  for (int q = 0; q < OCT_B; ++q) {
+    uint64_t acc = mad_wide(pan[q], zp[q], 0ull);
+#pragma unroll
+    for (int s2 = 0; s2 < q; ++s2) acc = mad_wide(t[s2], vr[q * (q - 1) / 2 + s2], acc);
+    t[q] = oct_reduce(acc, m);
+    tau[q] = mont(t[q], ze[q], m);
+  }
+}
+
 template <class Src, bool DFT8, int LPM>
 __global__ void __launch_bounds__(256)
 det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t nodes,
@@ -203,10 +223,11 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
   const unsigned omask = (LPM == 32 ? 0xffffffffu : ((1u << LPM) - 1u)) << (grp * LPM);
   const int my = warp * GPW + grp;                     // matrix slot within the CTA
   uint32_t* A = mats + (size_t)my * g.MS;
-  uint32_t* V = A + r * S;                             // [B][B]  V[s][S] (R-scaled, negated)
-  uint32_t* ZPR = V + OCT_B * OCT_B;                   // [B+1]   prod_{s<S} z_s * R
+  uint32_t* PB = A + r * S;                            // [B][16] panel [D | I], then V[s][S] (R-scaled, negated)
+  uint32_t* ZPR = PB + OCT_B * PBW;                    // [B+1]   prod_{s<S} z_s * R
   uint32_t* ZETAR = ZPR + OCT_B + 1;                   // [B]     prod_{s<s'<B} z_s' * R
   uint32_t* ZR = ZETAR + OCT_B;                        // [B]     z_s * R
+  uint32_t* CC = ZR + OCT_B;                           // [B][B]  -R^2 * C (U12 transform)
   const uint32_t p = m.p;
   const int cend = (r + 3) & ~3;
 
@@ -230,68 +251,94 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
     bool ok = true;
     for (int K = 0; K < r && ok; K += OCT_B) {
       const int Bk = (r - K) < OCT_B ? (r - K) : OCT_B;
-      // ---------------- P phase: pivot rows ----------------
+      // ---------------- P phase: factor the augmented diagonal block [D | I] ----------------
+      // PB = [D | I] (8 x 16, dense): D = rows/cols K..K+Bk-1 of the matrix, I = identity.
+      // Division-free rank-1 steps leave, for every pivot row s, its final values
+      // restricted to the block (PB[s][s+1..7]) and the transform C with
+      // final row s = sum_{q<=s} C[s][q] * original row K+q (PB[s][8..15]);
+      // every finished pivot row is stored as NPR (-R * value).
+      for (int w = l; w < OCT_B * PBW; w += LPM) {
+        const int q = w / PBW, c = w - q * PBW;
+        uint32_t v = 0;
+        if (q < Bk) v = c < Bk ? A[(K + q) * S + K + c] : (c - OCT_B == q ? 1u : 0u);
+        PB[w] = v;
+      }
+      __syncwarp(omask);
       for (int s = 0; s < Bk; ++s) {
-        const int k = K + s;
-        const uint32_t z = A[k * S + k];
+        const uint32_t z = PB[s * PBW + s];
         if (z == 0) { ok = false; break; }
         const uint32_t zR = to_mont(z, m);
         preR = mont(preR, zR, m);
-        if (k + 1 < r) inflR = mont(inflR, preR, m);
+        if (K + s + 1 < r) inflR = mont(inflR, preR, m);
         if (l == 0) ZR[s] = zR;
-        // 4-column chunks from a0 (<= k+1); columns <= k keep their value
-        const int a0 = (k + 1) & ~3;
-        const int nch = (cend - a0) >> 2;
-        uint32_t* prow = A + k * S;
-        // row k is final: NPR_s[c] = -R * prow_s[c] for c > k
+        const int a0 = (s + 1) & ~3;
+        const int nch = (PBW - a0) >> 2;
+        uint32_t* prow = PB + s * PBW;
         for (int ch = l; ch < nch; ch += LPM) {
           const int c = a0 + 4 * ch;
           uint4 v = *reinterpret_cast<const uint4*>(prow + c);
           uint32_t t0 = to_mont(v.x, m), t1 = to_mont(v.y, m), t2 = to_mont(v.z, m), t3 = to_mont(v.w, m);
           t0 = t0 ? p - t0 : 0u; t1 = t1 ? p - t1 : 0u; t2 = t2 ? p - t2 : 0u; t3 = t3 ? p - t3 : 0u;
-          if (c + 0 > k) v.x = t0;
-          if (c + 1 > k) v.y = t1;
-          if (c + 2 > k) v.z = t2;
-          if (c + 3 > k) v.w = t3;
+          if (c + 0 > s) v.x = t0;
+          if (c + 1 > s) v.y = t1;
+          if (c + 2 > s) v.z = t2;
+          if (c + 3 > s) v.w = t3;
           *reinterpret_cast<uint4*>(prow + c) = v;
         }
         __syncwarp(omask);
-        // pending pivot rows j in (k, K+Bk): rank-1 division-free update
-        //   row_j <- z*row_j - row_j[k]*prow  ==  REDC(row_j*zR + row_j[k]*NPR)
-        const int items = (K + Bk - k - 1) * nch;
-        if (items > 0) {
-          const int dj = LPM / nch, dc = LPM - dj * nch;
-          int jj = l / nch, cc = l - jj * nch;
-          for (int idx = l; idx < items; idx += LPM) {
-            uint32_t* rj = A + (k + 1 + jj) * S;
-            const int c = a0 + 4 * cc;
-            const uint32_t tj = rj[k];
-            const uint4 np = *reinterpret_cast<const uint4*>(prow + c);
-            uint4 a = *reinterpret_cast<const uint4*>(rj + c);
-            const uint32_t n0 = oct_reduce(mad_wide(tj, np.x, mad_wide(a.x, zR, 0ull)), m);
-            const uint32_t n1 = oct_reduce(mad_wide(tj, np.y, mad_wide(a.y, zR, 0ull)), m);
-            const uint32_t n2 = oct_reduce(mad_wide(tj, np.z, mad_wide(a.z, zR, 0ull)), m);
-            const uint32_t n3 = oct_reduce(mad_wide(tj, np.w, mad_wide(a.w, zR, 0ull)), m);
-            if (c + 0 > k) a.x = n0;
-            if (c + 1 > k) a.y = n1;
-            if (c + 2 > k) a.z = n2;
-            if (c + 3 > k) a.w = n3;
-            *reinterpret_cast<uint4*>(rj + c) = a;
-            jj += dj;
-            cc += dc;
-            if (cc >= nch) { cc -= nch; ++jj; }
-          }
+        const int items = (Bk - 1 - s) * nch;
+        for (int idx = l; idx < items; idx += LPM) {
+          const int jj = idx / nch, cc = idx - jj * nch;   // nch <= 4: cheap
+          uint32_t* rj = PB + (s + 1 + jj) * PBW;
+          const int c = a0 + 4 * cc;
+          const uint32_t tj = rj[s];
+          const uint4 np = *reinterpret_cast<const uint4*>(prow + c);
+          uint4 a = *reinterpret_cast<const uint4*>(rj + c);
+          const uint32_t n0 = oct_reduce(mad_wide(tj, np.x, mad_wide(a.x, zR, 0ull)), m);
+          const uint32_t n1 = oct_reduce(mad_wide(tj, np.y, mad_wide(a.y, zR, 0ull)), m);
+          const uint32_t n2 = oct_reduce(mad_wide(tj, np.z, mad_wide(a.z, zR, 0ull)), m);
+          const uint32_t n3 = oct_reduce(mad_wide(tj, np.w, mad_wide(a.w, zR, 0ull)), m);
+          if (c + 0 > s) a.x = n0;
+          if (c + 1 > s) a.y = n1;
+          if (c + 2 > s) a.z = n2;
+          if (c + 3 > s) a.w = n3;
+          *reinterpret_cast<uint4*>(rj + c) = a;
         }
         __syncwarp(omask);
       }
       if (!ok) break;
       if (K + OCT_B >= r) break;       // no trailing rows: elimination done
+      // ---------------- U12: the pivot rows right of the block, all in one pass ----------------
+      //   NPR_s[c] = -R * sum_{q<=s} C[s][q] a[K+q][c] = REDC(sum_q CC[s][q] a[K+q][c]),
+      //   CC = -R^2 C mod p = to_mont(stored -R*C)
+      for (int w = l; w < OCT_B * OCT_B; w += LPM) CC[w] = to_mont(PB[(w / OCT_B) * PBW + OCT_B + (w % OCT_B)], m);
+      __syncwarp(omask);
+      {
+        uint32_t cc[OCT_B * (OCT_B + 1) / 2];
+#pragma unroll
+        for (int s = 0; s < OCT_B; ++s)
+#pragma unroll
+          for (int q = 0; q <= s; ++q) cc[s * (s + 1) / 2 + q] = CC[s * OCT_B + q];
+        for (int c = K + OCT_B + l; c < r; c += LPM) {
+          uint32_t a[OCT_B];
+#pragma unroll
+          for (int q = 0; q < OCT_B; ++q) a[q] = A[(K + q) * S + c];
+#pragma unroll
+          for (int s = 0; s < OCT_B; ++s) {
+            uint64_t acc = 0;
+#pragma unroll
+            for (int q = 0; q <= s; ++q) acc = mad_wide(cc[s * (s + 1) / 2 + q], a[q], acc);
+            A[(K + s) * S + c] = oct_reduce(acc, m);
+          }
+        }
+      }
       // ---------------- block scalars (lane q <-> pivot q) ----------------
+      // V[q][s] = NPR_q[K+s] * prod_{q<s'<s} z_s'  (in place in PB, q < s < 8)
       if (l < OCT_B) {
         const int q = l;
         uint32_t zz = m.r1;            // prod_{q<s'<s} z_s' * R
         for (int s = q + 1; s < OCT_B; ++s) {
-          V[q * OCT_B + s] = mont(A[(K + q) * S + K + s], zz, m);
+          PB[q * PBW + s] = mont(PB[q * PBW + s], zz, m);
           zz = mont(zz, ZR[s], m);
         }
         ZETAR[q] = zz;
@@ -313,23 +360,13 @@ det_octet_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, in
         zp[q] = ZPR[q];
         ze[q] = ZETAR[q];
 #pragma unroll
-        for (int s2 = 0; s2 < q; ++s2) vr[q * (q - 1) / 2 + s2] = V[s2 * OCT_B + q];
+        for (int s2 = 0; s2 < q; ++s2) vr[q * (q - 1) / 2 + s2] = PB[s2 * PBW + q];
       }
       const int half = l >> 3;
       for (int i = c0 + (l & 7); i < r; i += 8) {
         uint32_t* row = A + i * S;
-        uint32_t t[OCT_B], tau[OCT_B];
-        const uint4 pa = *reinterpret_cast<const uint4*>(row + K);      // panel of row i
-        const uint4 pb = *reinterpret_cast<const uint4*>(row + K + 4);
-        const uint32_t pan[OCT_B] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
-#pragma unroll
-        for (int q = 0; q < OCT_B; ++q) {
-          uint64_t acc = mad_wide(pan[q], zp[q], 0ull);
-#pragma unroll
-          for (int s2 = 0; s2 < q; ++s2) acc = mad_wide(t[s2], vr[q * (q - 1) / 2 + s2], acc);
-          t[q] = oct_reduce(acc, m);
-          tau[q] = mont(t[q], ze[q], m);
-        }
+        uint32_t tau[OCT_B];
+        oct_chain(row + K, zp, vr, ze, m, tau);
         for (int c = c0 + 4 * half; c < cend; c += 4 * HALVES) {
           const uint4 a4 = *reinterpret_cast<const uint4*>(row + c);
           uint64_t a0 = mad_wide(a4.x, zpr, 0ull), a1 = mad_wide(a4.y, zpr, 0ull);
