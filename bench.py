@@ -320,7 +320,7 @@ def run_ours(args):
         "matrices_n3_per_s": value * r ** 3,
         "e2e": {"value": e2e, "unit": "dets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e_ms / args.steps},
-        "roofline": {"bound": "int", "kernel": "det_octet_kernel<FusedSrc> (eval + elimination)",
+        "roofline": {"bound": "int", "kernel": "det_gj_kernel<FusedSrc> (eval + elimination)",
                      "achieved": achieved / 1e9, "peak": peak_delayed / 1e9, "unit": "Gupd/s",
                      "frac": achieved / peak_delayed, "traffic": None,
                      "peak_kind": "measured now: delayed 64-bit MAC + REDC primitive (pdb_mulmod_peak v1)",

@@ -17,9 +17,11 @@
 // The fast kernels only take diagonal pivots; a matrix whose diagonal pivot
 // vanishes is appended to a node list and recomputed by det_robust, so every
 // input (singular, structured, permuted) gets the exact answer.
+#include <string>
 #include <vector>
 #include "pdb_internal.cuh"
 #include "det_octet.cuh"
+#include "det_gj.cuh"
 
 namespace pdb {
 
@@ -168,7 +170,75 @@ int robust_slots(int r) {
 
 size_t det_scratch_bytes(int r, int64_t nodes) {
   const size_t robust_threads = robust_slots(r);
-  return 256 + sizeof(int64_t) * (size_t)nodes + sizeof(uint32_t) * (size_t)r * r * robust_threads;
+  return 256 + sizeof(int64_t) * (size_t)nodes + sizeof(uint32_t) * ((size_t)nodes + 3) +
+         sizeof(uint32_t) * (size_t)r * r * robust_threads;
+}
+
+// PDB_DET_KERNEL=octet selects the previous 8-lane kernel (comparison only).
+static bool use_octet() {
+  static const char* env = getenv("PDB_DET_KERNEL");
+  return env && std::string(env) == "octet";
+}
+
+// 2^(32 r) mod p: the Montgomery scale of an r x r determinant.
+static uint32_t mont_scale(const Mod32& m, int r) {
+  uint64_t acc = 1 % m.p, b = m.r1;
+  for (int e = r; e; e >>= 1) {
+    if (e & 1) acc = (uint64_t)((unsigned __int128)acc * b % m.p);
+    b = (uint64_t)((unsigned __int128)b * b % m.p);
+  }
+  return (uint32_t)acc;
+}
+
+template <class Src, bool DFT8, int LPM>
+static int launch_gj_geom(PrimeCtx* ctx, const GjGeom& g, Src src, const int32_t* ids, int64_t node_lo,
+                          int64_t nodes, uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn,
+                          cudaStream_t st) {
+  const size_t smem = gj_smem(g);
+  if (cudaFuncSetAttribute(det_gj_kernel<Src, DFT8, LPM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess)
+    return check_launch("det_gj attribute");
+  int ctas_per_sm = 0;
+  const int threads = g.M * LPM;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, det_gj_kernel<Src, DFT8, LPM>, threads, smem);
+  if (ctas_per_sm < 1) ctas_per_sm = 1;
+  const int64_t iters = DFT8 ? nodes / g.M : (nodes + g.M - 1) / g.M;
+  const int64_t cap = (int64_t)ctx->sms * ctas_per_sm;
+  const int grid = (int)(iters < cap ? iters : cap);
+  if (grid < 1) return 0;
+  det_gj_kernel<Src, DFT8, LPM><<<grid, threads, smem, st>>>(src, ids, node_lo, nodes, out, den, fc, fn, g, ctx->m);
+  count_launch();
+  if (int rc = check_launch("det_gj")) return rc;
+  const int64_t fblocks = (nodes + 255) / 256;
+  const int fgrid = (int)(fblocks < (int64_t)ctx->sms * 8 ? fblocks : (int64_t)ctx->sms * 8);
+  det_gj_finalize<<<fgrid, 256, 0, st>>>(out, den, nodes, mont_scale(ctx->m, g.r), ctx->m);
+  count_launch();
+  return check_launch("det_gj_finalize");
+}
+
+template <class Src, bool DFT8>
+static int launch_gj_lpm(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int64_t node_lo, int64_t nodes,
+                         uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
+  const int lpm = gj_lpm(r);
+  if (lpm == 32)
+    return launch_gj_geom<Src, DFT8, 32>(ctx, gj_pick(r, 32, DFT8), src, ids, node_lo, nodes, out, den, fc, fn, st);
+  if (lpm == 16)
+    return launch_gj_geom<Src, DFT8, 16>(ctx, gj_pick(r, 16, DFT8), src, ids, node_lo, nodes, out, den, fc, fn, st);
+  return launch_gj_geom<Src, DFT8, 8>(ctx, gj_pick(r, 8, DFT8), src, ids, node_lo, nodes, out, den, fc, fn, st);
+}
+
+static int launch_gj(PrimeCtx* ctx, int r, StagedSrc src, const int32_t* ids, int64_t node_lo, int64_t nodes,
+                     uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
+  return launch_gj_lpm<StagedSrc, false>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
+}
+
+static int launch_gj(PrimeCtx* ctx, int r, FusedSrc src, const int32_t* ids, int64_t node_lo, int64_t nodes,
+                     uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
+  const GjGeom g = gj_pick(r, gj_lpm(r), true);
+  const bool dft8 = src.E <= 8 && src.NL >= 8 && src.NL % (8 * g.U) == 0 && node_lo % src.NL == 0 &&
+                    nodes % src.NL == 0;
+  if (dft8) return launch_gj_lpm<FusedSrc, true>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
+  return launch_gj_lpm<FusedSrc, false>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
 }
 
 template <class Src>
@@ -185,19 +255,24 @@ int det_run(PrimeCtx* ctx, Src src, const int32_t* ids, int r, int64_t node_lo, 
   }
   char* base = static_cast<char*>(scratch);
   FlagList flags{reinterpret_cast<unsigned long long*>(base), reinterpret_cast<int64_t*>(base + 256)};
-  uint32_t* mats = reinterpret_cast<uint32_t*>(base + 256 + sizeof(int64_t) * (size_t)nodes);
+  uint32_t* den = reinterpret_cast<uint32_t*>(base + 256 + sizeof(int64_t) * (size_t)nodes);
+  uint32_t* mats = den + (((size_t)nodes + 3) & ~size_t(3));
   const Mod32 m = ctx->m;
   const int slots = robust_slots(r);
   bool fast = false;
   if (cudaMemsetAsync(flags.count, 0, sizeof(unsigned long long), st) != cudaSuccess)
     return check_launch("det memset");
-  if (r <= 8) {
+  if (r <= 8 && m.odd()) {
     int64_t blocks = (nodes + 127) / 128;
     int grid = (int)(blocks < (int64_t)ctx->sms * 32 ? blocks : (int64_t)ctx->sms * 32);
     launch_small(r, src, ids, node_lo, nodes, out, flags, m, grid, st);
     fast = true;
   } else if (m.fast()) {
-    if (launch_octet(ctx, r, src, ids, node_lo, nodes, out, flags.count, flags.nodes, st) == 0) fast = true;
+    if (use_octet()) {
+      if (launch_octet(ctx, r, src, ids, node_lo, nodes, out, flags.count, flags.nodes, st) == 0) fast = true;
+    } else if (launch_gj(ctx, r, src, ids, node_lo, nodes, out, den, flags.count, flags.nodes, st) == 0) {
+      fast = true;
+    }
   }
   if (int rc = check_launch("det fast path")) return rc;
   if (fast) {

@@ -23,7 +23,8 @@ struct Mod32 {
   uint32_t r1s;      // Shoup companion of r1
   uint64_t m64;      // floor(2^64 / p)   (Barrett for 64-bit products)
 
-  PDB_HD bool fast() const { return p < (1u << 30); }
+  PDB_HD bool fast() const { return p < (1u << 30) && (p & 1u); }   // Montgomery needs odd p
+  PDB_HD bool odd() const { return (p & 1u) != 0; }
 };
 
 PDB_HD uint32_t umulhi32(uint32_t a, uint32_t b) {

@@ -104,7 +104,7 @@ def test_det_matches_reference_golden(cuda):
     assert n > 40
 
 
-@pytest.mark.parametrize("r", [4, 9, 16, 17, 33, 40, 64])
+@pytest.mark.parametrize("r", [4, 9, 10, 12, 14, 15, 16, 17, 23, 24, 25, 32, 33, 40, 48, 56, 63, 64])
 def test_det_random_vs_oracle_with_zero_pivots(cuda, r):
     spec = find_fourier_primes(8, 1, start=10**9, min_count=1)[0]
     rng = np.random.default_rng(r)
@@ -117,6 +117,18 @@ def test_det_random_vs_oracle_with_zero_pivots(cuda, r):
     grids = [mats[:, e // r, e % r] for e in range(r * r)]
     got = det_grid(grids, r, spec)
     assert got.tolist() == O.det_grid(grids, r, spec.p).tolist()
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 97, 65537])
+def test_det_tiny_and_small_primes(cuda, p):
+    """Even p has no Montgomery form: such primes take the robust kernel; odd
+    small primes exercise zero pivots on the fast paths constantly."""
+    spec = PrimeSpec(p, p - 1, 0, 1)
+    rng = np.random.default_rng(p)
+    for r in (3, 8, 10, 24):
+        mats = rng.integers(0, p, (300, r, r))
+        grids = [mats[:, e // r, e % r] for e in range(r * r)]
+        assert det_grid(grids, r, spec).tolist() == O.det_grid(grids, r, p).tolist(), (p, r)
 
 
 def test_det_dedup_ids_and_31bit_prime(cuda):
