@@ -74,11 +74,13 @@ int32_t pdb_det_batch_u32(pdb_prime_ctx* ctx, const uint32_t* grids, int64_t gri
                           const int32_t* entry_ids, int32_t r, int64_t node_lo, int64_t nodes,
                           uint32_t* out, void* scratch, size_t scratch_bytes, void* stream);
 
-/* Same, with the entries evaluated on the fly: partial[(e*outer + o)*ncoef + l]
- * holds entry e transformed along every axis but the last, l-th coefficient of
- * the last variable; node = o * n_last + c is evaluated at w_{n_last}^c. */
+/* Same, with the entries evaluated on the fly: partial[(o*ncoef + l)*entries + e]
+ * holds entry e (of `entries` unique ones) transformed along every axis but the
+ * last, l-th coefficient of the last variable; node = o * n_last + c is
+ * evaluated at w_{n_last}^c.  (Layout [outer][ncoef][entries]: the entries are
+ * innermost so the kernel's fills read coalesced rows.) */
 int32_t pdb_eval_det_fused_u32(pdb_prime_ctx* ctx, const uint32_t* partial, int64_t outer,
-                               int32_t ncoef, int32_t n_last, const int32_t* entry_ids, int32_t r,
+                               int32_t ncoef, int32_t entries, int32_t n_last, const int32_t* entry_ids, int32_t r,
                                int64_t node_lo, int64_t nodes, uint32_t* out, void* scratch,
                                size_t scratch_bytes, void* stream);
 

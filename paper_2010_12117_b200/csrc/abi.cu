@@ -6,7 +6,7 @@
 
 #include "../../include/polydet_b200.h"
 #include "pdb_internal.cuh"
-#include "det_octet.cuh"
+
 
 struct pdb_prime_ctx : pdb::PrimeCtx {};
 
@@ -157,7 +157,7 @@ __global__ void peak_delayed(uint32_t* out, uint32_t seed, Mod32 m, int iters) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i] += (uint64_t)tau[q] * (np[q] ^ i);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = oct_reduce(acc[i], m);
+    for (int i = 0; i < 4; ++i) a[i] = csub(csub(redc(acc[i], m), 2u * m.p), m.p);
   }
   uint32_t s = 0;
 #pragma unroll
@@ -250,13 +250,13 @@ int32_t pdb_det_batch_u32(pdb_prime_ctx* ctx, const uint32_t* grids, int64_t gri
 }
 
 int32_t pdb_eval_det_fused_u32(pdb_prime_ctx* ctx, const uint32_t* partial, int64_t outer,
-                               int32_t ncoef, int32_t n_last, const int32_t* entry_ids, int32_t r,
+                               int32_t ncoef, int32_t entries, int32_t n_last, const int32_t* entry_ids, int32_t r,
                                int64_t node_lo, int64_t nodes, uint32_t* out, void* scratch,
                                size_t scratch_bytes, void* stream) {
-  if (!ctx || ncoef < 1) { set_error("invalid fused arguments"); return -2; }
+  if (!ctx || ncoef < 1 || entries < 1) { set_error("invalid fused arguments"); return -2; }
   const Twiddles* T = ctx_twiddles(ctx, n_last);
   if (!T) return -2;
-  FusedSrc src{partial, outer, ncoef, n_last, T->full, T->full_s, ctx->m.p};
+  FusedSrc src{partial, outer, ncoef, entries, n_last, T->full, T->full_s, ctx->m.p};
   return det_run(ctx, src, entry_ids, r, node_lo, nodes, out, scratch, scratch_bytes, (cudaStream_t)stream);
 }
 

@@ -6,10 +6,11 @@
 //
 //  * det_small<R>   R <= 8: one lane per matrix, the matrix in registers,
 //                   division-free elimination with diagonal pivots.
-//  * det_octet      9 <= r <= 64 and p < 2^30: eight lanes per matrix, the
-//                   matrix in shared memory, blocked division-free elimination
-//                   with delayed (64-bit accumulate + Montgomery) reduction
-//                   (det_octet.cuh).
+//  * det_gj         9 <= r <= 64 and odd p < 2^30: a lane group (8/16/32
+//                   lanes) per matrix in shared memory, blocked Schur
+//                   complements with an 8x8 Gauss-Jordan pivot block and
+//                   delayed (64-bit accumulate + Montgomery) reduction
+//                   (det_gj.cuh).
 //  * det_robust     any r <= 64, any p < 2^31: one thread per matrix with the
 //                   reference's exact pivot rule (first nonzero column of row
 //                   i, determinant.py:136-169) and full division-free updates.
@@ -20,7 +21,6 @@
 #include <string>
 #include <vector>
 #include "pdb_internal.cuh"
-#include "det_octet.cuh"
 #include "det_gj.cuh"
 
 namespace pdb {
@@ -174,12 +174,6 @@ size_t det_scratch_bytes(int r, int64_t nodes) {
          sizeof(uint32_t) * (size_t)r * r * robust_threads;
 }
 
-// PDB_DET_KERNEL=octet selects the previous 8-lane kernel (comparison only).
-static bool use_octet() {
-  static const char* env = getenv("PDB_DET_KERNEL");
-  return env && std::string(env) == "octet";
-}
-
 // 2^(32 r) mod p: the Montgomery scale of an r x r determinant.
 static uint32_t mont_scale(const Mod32& m, int r) {
   uint64_t acc = 1 % m.p, b = m.r1;
@@ -268,11 +262,7 @@ int det_run(PrimeCtx* ctx, Src src, const int32_t* ids, int r, int64_t node_lo, 
     launch_small(r, src, ids, node_lo, nodes, out, flags, m, grid, st);
     fast = true;
   } else if (m.fast()) {
-    if (use_octet()) {
-      if (launch_octet(ctx, r, src, ids, node_lo, nodes, out, flags.count, flags.nodes, st) == 0) fast = true;
-    } else if (launch_gj(ctx, r, src, ids, node_lo, nodes, out, den, flags.count, flags.nodes, st) == 0) {
-      fast = true;
-    }
+    if (launch_gj(ctx, r, src, ids, node_lo, nodes, out, den, flags.count, flags.nodes, st) == 0) fast = true;
   }
   if (int rc = check_launch("det fast path")) return rc;
   if (fast) {

@@ -58,6 +58,14 @@ __device__ __forceinline__ uint32_t gj_red(uint64_t acc, const Mod32& m) {
   return csub(csub(v, 2u * m.p), m.p);
 }
 
+// REDC of <= 2 products of canonical residues: output < 1.5 p, one subtraction.
+__device__ __forceinline__ uint32_t gj_red2(uint64_t acc, const Mod32& m) { return csub(redc(acc, m), m.p); }
+
+// Montgomery product of canonical a, b (Montgomery forms stay Montgomery forms).
+__device__ __forceinline__ uint32_t gj_mont(uint32_t a, uint32_t b, const Mod32& m) {
+  return gj_red2(mad_wide(a, b, 0ull), m);
+}
+
 __device__ __forceinline__ void gj_cp_async4(uint32_t* dst, const uint32_t* src) {
   unsigned s = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src));
@@ -120,102 +128,185 @@ __device__ __forceinline__ void gj_fill(const FusedSrc& src, uint32_t* mats, con
                                                   : (pi.i == pi.j ? one : 0u);
 }
 
-// 8 nodes per thread: f(o*NL + u + (NL/8) v) = sum_l (T_l w^(u l)) w8^(l v), an
-// 8-point DIT transform of the twisted coefficients (E <= 8).
-__device__ __forceinline__ void gj_fill_dft8(const FusedSrc& src, uint32_t* mats, const GjGeom& g, const int32_t* ids,
-                                             int64_t it, int64_t node_lo, uint32_t one) {
-  const int r = g.r, RP = g.RP, S = g.S, U = g.U, NL = src.NL, E = src.E;
+// Radix-2 butterfly (x, y) -> (x + y, x - y); ZERO: y is known to be 0.
+template <bool ZERO>
+__device__ __forceinline__ void gj_bf(uint32_t& x, uint32_t& y, uint32_t p) {
+  if constexpr (ZERO) {
+    y = x;
+  } else {
+    const uint32_t t = y;
+    y = sub_mod(x, t, p);
+    x = add_mod(x, t, p);
+  }
+}
+
+// X[v] = sum_{l<E} c_l w^(u l) w8^(l v), v < 8: twist, then an 8-point DIT
+// transform whose first stage is trivial for the coefficient slots >= E.
+template <int E>
+__device__ __forceinline__ void gj_dft8(const uint32_t (&c)[E], const uint32_t* tw, const uint32_t* tws,
+                                        const uint32_t (&w)[4], const uint32_t (&ws)[4], uint32_t p,
+                                        uint32_t (&x)[8]) {
+  uint32_t q[8];
+  q[0] = c[0];
+#pragma unroll
+  for (int l = 1; l < 8; ++l) q[l] = l < E ? shoup_mul(c[l < E ? l : 0], tw[l], tws[l], p) : 0u;
+  // bit-reversed order
+  x[0] = q[0]; x[1] = q[4]; x[2] = q[2]; x[3] = q[6]; x[4] = q[1]; x[5] = q[5]; x[6] = q[3]; x[7] = q[7];
+  gj_bf<(4 >= E)>(x[0], x[1], p);
+  gj_bf<(6 >= E)>(x[2], x[3], p);
+  gj_bf<(5 >= E)>(x[4], x[5], p);
+  gj_bf<(7 >= E)>(x[6], x[7], p);
+  uint32_t t;
+  gj_bf<false>(x[0], x[2], p);
+  t = shoup_mul(x[3], w[2], ws[2], p); x[3] = t; gj_bf<false>(x[1], x[3], p);
+  gj_bf<false>(x[4], x[6], p);
+  t = shoup_mul(x[7], w[2], ws[2], p); x[7] = t; gj_bf<false>(x[5], x[7], p);
+  gj_bf<false>(x[0], x[4], p);
+  t = shoup_mul(x[5], w[1], ws[1], p); x[5] = t; gj_bf<false>(x[1], x[5], p);
+  t = shoup_mul(x[6], w[2], ws[2], p); x[6] = t; gj_bf<false>(x[2], x[6], p);
+  t = shoup_mul(x[7], w[3], ws[3], p); x[7] = t; gj_bf<false>(x[3], x[7], p);
+}
+
+// 8 nodes per thread: f(o*NL + u + (NL/8) v) = sum_l (T_l w^(u l)) w8^(l v) for
+// the slot v*U + uu.  The coefficients of one outer index o are the slab
+// part[o][l][e] (entries innermost): consecutive threads read consecutive
+// entries; two positions are kept in flight per thread.
+template <int E>
+__device__ __forceinline__ void gj_fill_dft8_e(const FusedSrc& src, uint32_t* mats, const GjGeom& g,
+                                               const int32_t* ids, int64_t it, int64_t node_lo, uint32_t one) {
+  const int r = g.r, RP = g.RP, S = g.S, U = g.U, NL = src.NL, k = src.k;
   const uint32_t p = src.p;
   const int per_o = NL / (8 * U);
   const int64_t o = (node_lo / NL) + it / per_o;
   const int ublk = (int)(it % per_o);
   const int step8 = NL / 8;
-  const uint32_t w1 = __ldg(src.xs + step8), w1s = __ldg(src.xss + step8);
-  const uint32_t w2 = __ldg(src.xs + 2 * step8), w2s = __ldg(src.xss + 2 * step8);
-  const uint32_t w3 = __ldg(src.xs + 3 * step8), w3s = __ldg(src.xss + 3 * step8);
+  uint32_t w[4], ws[4];
+#pragma unroll
+  for (int v = 1; v < 4; ++v) { w[v] = __ldg(src.xs + v * step8); ws[v] = __ldg(src.xss + v * step8); }
+  w[0] = ws[0] = 0;
   const int uu = threadIdx.x % U;
   uint32_t tw[8], tws[8];
   {
     const int u = ublk * U + uu;
-    int k = 0;
+    int kk = 0;
 #pragma unroll
-    for (int ll = 0; ll < 8; ++ll) {
-      tw[ll] = __ldg(src.xs + k);
-      tws[ll] = __ldg(src.xss + k);
-      k += u;
-      if (k >= NL) k -= NL;
+    for (int l = 0; l < 8; ++l) {
+      if (l < E) { tw[l] = __ldg(src.xs + kk); tws[l] = __ldg(src.xss + kk); }
+      else { tw[l] = tws[l] = 0; }
+      kk += u;
+      if (kk >= NL) kk -= NL;
     }
   }
   const size_t ms = (size_t)U * g.MS;   // slot v*U + uu
   uint32_t* base = mats + (size_t)uu * g.MS;
+  const uint32_t* slab = src.part + o * (int64_t)E * k;
   GjPos pi(threadIdx.x / U, blockDim.x / U, RP);
-  for (; pi.i < RP; pi.next()) {
-    const int i = pi.i, j = pi.j;
-    uint32_t* d = base + i * S + j;
-    if (i >= r || j >= r) {
-      const uint32_t c = i == j ? one : 0u;
+  while (pi.i < RP) {
+    const int ia = pi.i, ja = pi.j;
+    pi.next();
+    const int ib = pi.i, jb = pi.j;
+    const bool hb = ib < RP;
+    if (hb) pi.next();
+    const bool ra = ia < r && ja < r, rb = hb && ib < r && jb < r;
+    const uint32_t* pa = slab + (ra ? ids[ia * r + ja] : 0);
+    const uint32_t* pb = slab + (rb ? ids[ib * r + jb] : 0);
+    uint32_t ca[E], cb[E];
+#pragma unroll
+    for (int l = 0; l < E; ++l) { ca[l] = __ldg(pa + (int64_t)l * k); cb[l] = __ldg(pb + (int64_t)l * k); }
+    uint32_t x[8];
+    uint32_t* d = base + ia * S + ja;
+    if (ra) {
+      gj_dft8<E>(ca, tw, tws, w, ws, p, x);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) d[v * ms] = x[v];
+    } else {
+      const uint32_t c = ia == ja ? one : 0u;
 #pragma unroll
       for (int v = 0; v < 8; ++v) d[v * ms] = c;
-      continue;
     }
-    const uint32_t* a = src.part + ((int64_t)ids[i * r + j] * src.outer + o) * E;
-    uint32_t q[8];
-    q[0] = __ldg(a);
+    if (hb) {
+      d = base + ib * S + jb;
+      if (rb) {
+        gj_dft8<E>(cb, tw, tws, w, ws, p, x);
 #pragma unroll
-    for (int ll = 1; ll < 8; ++ll) q[ll] = ll < E ? shoup_mul(__ldg(a + ll), tw[ll], tws[ll], p) : 0u;
-    uint32_t x0 = q[0], x1 = q[4], x2 = q[2], x3 = q[6], x4 = q[1], x5 = q[5], x6 = q[3], x7 = q[7];
-    uint32_t t;
-    t = x1; x1 = sub_mod(x0, t, p); x0 = add_mod(x0, t, p);
-    t = x3; x3 = sub_mod(x2, t, p); x2 = add_mod(x2, t, p);
-    t = x5; x5 = sub_mod(x4, t, p); x4 = add_mod(x4, t, p);
-    t = x7; x7 = sub_mod(x6, t, p); x6 = add_mod(x6, t, p);
-    t = x2; x2 = sub_mod(x0, t, p); x0 = add_mod(x0, t, p);
-    t = shoup_mul(x3, w2, w2s, p); x3 = sub_mod(x1, t, p); x1 = add_mod(x1, t, p);
-    t = x6; x6 = sub_mod(x4, t, p); x4 = add_mod(x4, t, p);
-    t = shoup_mul(x7, w2, w2s, p); x7 = sub_mod(x5, t, p); x5 = add_mod(x5, t, p);
-    t = x4; x4 = sub_mod(x0, t, p); x0 = add_mod(x0, t, p);
-    t = shoup_mul(x5, w1, w1s, p); x5 = sub_mod(x1, t, p); x1 = add_mod(x1, t, p);
-    t = shoup_mul(x6, w2, w2s, p); x6 = sub_mod(x2, t, p); x2 = add_mod(x2, t, p);
-    t = shoup_mul(x7, w3, w3s, p); x7 = sub_mod(x3, t, p); x3 = add_mod(x3, t, p);
-    d[0] = x0; d[ms] = x1; d[2 * ms] = x2; d[3 * ms] = x3;
-    d[4 * ms] = x4; d[5 * ms] = x5; d[6 * ms] = x6; d[7 * ms] = x7;
+        for (int v = 0; v < 8; ++v) d[v * ms] = x[v];
+      } else {
+        const uint32_t c = ib == jb ? one : 0u;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) d[v * ms] = c;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void gj_fill_dft8(const FusedSrc& src, uint32_t* mats, const GjGeom& g, const int32_t* ids,
+                                             int64_t it, int64_t node_lo, uint32_t one) {
+  switch (src.E) {
+    case 1: gj_fill_dft8_e<1>(src, mats, g, ids, it, node_lo, one); break;
+    case 2: gj_fill_dft8_e<2>(src, mats, g, ids, it, node_lo, one); break;
+    case 3: gj_fill_dft8_e<3>(src, mats, g, ids, it, node_lo, one); break;
+    case 4: gj_fill_dft8_e<4>(src, mats, g, ids, it, node_lo, one); break;
+    case 5: gj_fill_dft8_e<5>(src, mats, g, ids, it, node_lo, one); break;
+    case 6: gj_fill_dft8_e<6>(src, mats, g, ids, it, node_lo, one); break;
+    case 7: gj_fill_dft8_e<7>(src, mats, g, ids, it, node_lo, one); break;
+    default: gj_fill_dft8_e<8>(src, mats, g, ids, it, node_lo, one); break;
   }
 }
 
 // ---- T pass: A22 <- c*A22 + A21*negM over TR x TC tiles ------------------------------
+template <int TC>
+__device__ __forceinline__ void gj_ld(const uint32_t* a, uint32_t (&v)[TC]) {
+  if constexpr (TC % 4 == 0) {
+#pragma unroll
+    for (int b = 0; b < TC; b += 4) {
+      const uint4 x = *reinterpret_cast<const uint4*>(a + b);
+      v[b] = x.x; v[b + 1] = x.y; v[b + 2] = x.z; v[b + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int b = 0; b < TC; b += 2) {
+      const uint2 x = *reinterpret_cast<const uint2*>(a + b);
+      v[b] = x.x; v[b + 1] = x.y;
+    }
+  }
+}
+
+template <int TC>
+__device__ __forceinline__ void gj_st(uint32_t* a, const uint32_t (&v)[TC]) {
+  if constexpr (TC % 4 == 0) {
+#pragma unroll
+    for (int b = 0; b < TC; b += 4) *reinterpret_cast<uint4*>(a + b) = make_uint4(v[b], v[b + 1], v[b + 2], v[b + 3]);
+  } else {
+#pragma unroll
+    for (int b = 0; b < TC; b += 2) *reinterpret_cast<uint2*>(a + b) = make_uint2(v[b], v[b + 1]);
+  }
+}
+
 template <int TR, int TC, int LPM>
 __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, uint32_t cR, int l, const Mod32& m) {
   const int c0 = K + GJ_B;
   const int ntc = mrem / TC;
   const int tiles = (mrem / TR) * ntc;
   const uint32_t* npr = A + K * S;    // negM rows K..K+7
+  int ti = l / ntc, tc = l - (l / ntc) * ntc;
+  const int dti = LPM / ntc, dtc = LPM - (LPM / ntc) * ntc;
   for (int w = l; w < tiles; w += LPM) {
-    const int ti = w / ntc, tc = w - ti * ntc;
     const int i0 = c0 + TR * ti, cc = c0 + TC * tc;
     uint32_t a21[TR][GJ_B];
     uint64_t acc[TR][TC];
 #pragma unroll
     for (int a = 0; a < TR; ++a) {
       const uint32_t* row = A + (i0 + a) * S;
-      const uint4 x = *reinterpret_cast<const uint4*>(row + K);
-      const uint4 y = *reinterpret_cast<const uint4*>(row + K + 4);
-      a21[a][0] = x.x; a21[a][1] = x.y; a21[a][2] = x.z; a21[a][3] = x.w;
-      a21[a][4] = y.x; a21[a][5] = y.y; a21[a][6] = y.z; a21[a][7] = y.w;
+      gj_ld<GJ_B>(row + K, a21[a]);
+      uint32_t v[TC];
+      gj_ld<TC>(row + cc, v);
 #pragma unroll
-      for (int b = 0; b < TC; b += 2) {
-        const uint2 v = *reinterpret_cast<const uint2*>(row + cc + b);
-        acc[a][b] = mad_wide(v.x, cR, 0ull);
-        acc[a][b + 1] = mad_wide(v.y, cR, 0ull);
-      }
+      for (int b = 0; b < TC; ++b) acc[a][b] = mad_wide(v[b], cR, 0ull);
     }
 #pragma unroll
     for (int q = 0; q < GJ_B; ++q) {
       uint32_t nm[TC];
-#pragma unroll
-      for (int b = 0; b < TC; b += 2) {
-        const uint2 v = *reinterpret_cast<const uint2*>(npr + q * S + cc + b);
-        nm[b] = v.x; nm[b + 1] = v.y;
-      }
+      gj_ld<TC>(npr + q * S + cc, nm);
 #pragma unroll
       for (int a = 0; a < TR; ++a)
 #pragma unroll
@@ -223,15 +314,13 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
     }
 #pragma unroll
     for (int a = 0; a < TR; ++a) {
-      uint32_t* row = A + (i0 + a) * S;
+      uint32_t v[TC];
 #pragma unroll
-      for (int b = 0; b < TC; b += 2) {
-        uint2 v;
-        v.x = gj_red(acc[a][b], m);
-        v.y = gj_red(acc[a][b + 1], m);
-        *reinterpret_cast<uint2*>(row + cc + b) = v;
-      }
+      for (int b = 0; b < TC; ++b) v[b] = gj_red(acc[a][b], m);
+      gj_st<TC>(A + (i0 + a) * S + cc, v);
     }
+    ti += dti; tc += dtc;
+    if (tc >= ntc) { tc -= ntc; ++ti; }
   }
 }
 
@@ -296,6 +385,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         for (int k = 0; k < EPL; ++k) v[k] = src_row[k];
       }
       uint32_t lam = one, zl = one, z7 = one;
+      bool zero = false;
 #pragma unroll
       for (int s = 0; s < GJ_B; ++s) {
         const uint32_t z = __shfl_sync(omask, v[s % EPL], s * LPR + s / EPL, LPM);
@@ -303,34 +393,29 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         uint32_t prow[EPL];
 #pragma unroll
         for (int k = 0; k < EPL; ++k) prow[k] = __shfl_sync(omask, v[k], s * LPR + l % LPR, LPM);
-        if (z == 0) { ok = false; break; }
-        if (pj == s) zl = lam;
-        const uint32_t nt = t ? p - t : 0u;
+        zero |= z == 0;
+        zl = pj == s ? lam : zl;
+        const uint32_t nt = p - t;   // in (0, p]: a valid multiplier for the 2-product REDC
 #pragma unroll
         for (int k = 0; k < EPL; ++k) {
-          const int cc = pc + k;
-          if (pj != s) {
-            const uint32_t a = cc == s ? 0u : v[k];
-            const uint32_t b = cc == s ? lam : prow[k];
-            v[k] = gj_red(mad_wide(z, a, mad_wide(nt, b, 0ull)), m);
-          } else if (cc == s) {
-            v[k] = lam;
-          }
+          const bool diag = pc + k == s;
+          const uint32_t nv = gj_red2(mad_wide(z, diag ? 0u : v[k], mad_wide(nt, diag ? lam : prow[k], 0ull)), m);
+          v[k] = pj != s ? nv : (diag ? lam : v[k]);
         }
-        if (s >= 1 && s <= 6) den = mont(den, lam, m);
+        if (s >= 1 && s <= 6) den = gj_mont(den, lam, m);
         if (s == GJ_B - 1) z7 = z;
-        lam = mont(lam, z, m);
+        lam = gj_mont(lam, z, m);
       }
-      if (!ok) break;
-      num = mont(num, z7, m);
+      if (zero) { ok = false; break; }
+      num = gj_mont(num, z7, m);
       if (mrem == 0) break;
       const uint32_t cR = lam;   // c = prod z_s
-      Q = mont(Q, cR, m);
-      C = mont(C, Q, m);
+      Q = gj_mont(Q, cR, m);
+      C = gj_mont(C, Q, m);
       // negX = -Z_{<j} E  ->  NX[pj][pc + k]
 #pragma unroll
       for (int k = 0; k < EPL; ++k) {
-        const uint32_t x = mont(v[k], zl, m);
+        const uint32_t x = gj_mont(v[k], zl, m);
         NX[pj * GJ_B + pc + k] = x ? p - x : 0u;
       }
       __syncwarp(omask);
@@ -384,11 +469,11 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
     if (l == 0) {
       if (ok) {
         // C^8
-        C = mont(C, C, m);
-        C = mont(C, C, m);
-        C = mont(C, C, m);
+        C = gj_mont(C, C, m);
+        C = gj_mont(C, C, m);
+        C = gj_mont(C, C, m);
         num_out[node] = num;
-        den_out[node] = mont(den, C, m);
+        den_out[node] = gj_mont(den, C, m);
       } else {
         den_out[node] = 0u;
         unsigned long long k = atomicAdd(flag_count, 1ull);

@@ -56,13 +56,16 @@ struct StagedSrc {
   }
 };
 
-// Fused: partially transformed entries [k][outer][E] (every axis but the last
-// already evaluated; E coefficient planes along the last axis).  The value of
-// entry e at node = o * NL + c is the degree-(E-1) polynomial in x = w_NL^c.
+// Fused: partially transformed entries [outer][E][k] (every axis but the last
+// already evaluated; E coefficient planes along the last axis; the k unique
+// entries innermost, so a CTA filling its matrices reads coalesced rows).
+// The value of entry e at node = o * NL + c is the degree-(E-1) polynomial in
+// x = w_NL^c with coefficients part[(o*E + l)*k + e].
 struct FusedSrc {
   const uint32_t* part;
   int64_t outer;
   int E;
+  int k;
   int NL;
   const uint32_t* xs;    // w^c, c < NL
   const uint32_t* xss;   // companions
@@ -70,10 +73,10 @@ struct FusedSrc {
   __device__ __forceinline__ uint32_t get(int e, int64_t node) const {
     int64_t o = node / NL;
     int c = (int)(node - o * NL);
-    const uint32_t* a = part + ((int64_t)e * outer + o) * E;
+    const uint32_t* a = part + o * E * (int64_t)k + e;
     uint32_t x = __ldg(xs + c), xc = __ldg(xss + c);
-    uint32_t v = __ldg(a + E - 1);
-    for (int l = E - 2; l >= 0; --l) v = add_mod(shoup_mul(v, x, xc, p), __ldg(a + l), p);
+    uint32_t v = __ldg(a + (int64_t)(E - 1) * k);
+    for (int l = E - 2; l >= 0; --l) v = add_mod(shoup_mul(v, x, xc, p), __ldg(a + (int64_t)l * k), p);
     return v;
   }
 };

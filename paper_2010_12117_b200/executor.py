@@ -139,7 +139,8 @@ class DevicePlan:
         else:
             self.E = max(t.shape[-1] for t in m.unique_entries)
             self.outer = self.nodes // self.shape[-1]
-            pos = [(e * self.outer + _flat(exps[:-1], self.shape[:-1])) * self.E + exps[-1]
+            # [outer][E][k]: entries innermost (coalesced fills in the det kernel)
+            pos = [(_flat(exps[:-1], self.shape[:-1]) * self.E + exps[-1]) * self.k + e
                    for e, exps in entries]
         self.mag = torch.from_numpy(mag.view(np.int32).copy()).to(device) if self.count else \
             torch.zeros(1, dtype=torch.int32, device=device)
@@ -260,9 +261,9 @@ def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
     work.zero_()
     if not dp.staged:
         native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, work)
-        dims = dp.shape[:-1] + (dp.E,)
-        ext = dp.ext[:-1] + [dp.E]
-        native.ntt_multi(ctx, work, dp.k, dims, ext, range(dp.vn - 1), False)
+        dims = dp.shape[:-1] + (dp.E, dp.k)
+        ext = dp.ext[:-1] + [dp.E, dp.k]
+        native.ntt_multi(ctx, work, 1, dims, ext, range(dp.vn - 1), False)
         return
     todo = []
     for eid in range(dp.k):
@@ -305,7 +306,7 @@ def _det_stage(dp: DevicePlan, ctx, work, det_buf, scratch, chunk, ws, pi, cfg):
         n_last = dp.shape[-1]
         for lo in range(0, dp.nodes, chunk):
             cnt = min(chunk, dp.nodes - lo)
-            native.eval_det_fused(ctx, work, dp.outer, dp.E, n_last, dp.ids, pl.r, lo, cnt,
+            native.eval_det_fused(ctx, work, dp.outer, dp.E, dp.k, n_last, dp.ids, pl.r, lo, cnt,
                                   det_buf[lo:lo + cnt], scratch)
     if dp.staged:   # fused mode has no det (or fft) units: it checkpoints per prime
         if ws is not None:

@@ -40,7 +40,7 @@ _SIGNATURES = {
     "pdb_det_scratch_bytes": (_c_size, [_c_i32, _c_i64]),
     "pdb_det_batch_u32": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i32, _c_i64, _c_i64, _c_vp,
                                    _c_vp, _c_size, _c_vp]),
-    "pdb_eval_det_fused_u32": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_vp, _c_i32, _c_i64,
+    "pdb_eval_det_fused_u32": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_vp, _c_i32, _c_i64,
                                         _c_i64, _c_vp, _c_vp, _c_size, _c_vp]),
     "pdb_condense_u32": (_c_i32, [_c_vp, _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_vp, _c_size, _c_vp]),
     "pdb_crt_limbs": (_c_i32, [_c_i32]),
@@ -182,10 +182,11 @@ def det_batch(ctx: PrimeContext, grids, grid_stride: int, ids, r: int, node_lo: 
                                 stream_handle(stream)), "det")
 
 
-def eval_det_fused(ctx: PrimeContext, partial, outer: int, ncoef: int, n_last: int, ids, r: int,
+def eval_det_fused(ctx: PrimeContext, partial, outer: int, ncoef: int, entries: int, n_last: int, ids, r: int,
                    node_lo: int, nodes: int, out, scratch, stream=None):
+    """partial: [outer][ncoef][entries] u32 (see include/polydet_b200.h)."""
     lib = load_library()
-    check(lib.pdb_eval_det_fused_u32(ctx.handle, ptr(partial), int(outer), int(ncoef), int(n_last),
+    check(lib.pdb_eval_det_fused_u32(ctx.handle, ptr(partial), int(outer), int(ncoef), int(entries), int(n_last),
                                      ptr(ids), int(r), int(node_lo), int(nodes), ptr(out), ptr(scratch),
                                      scratch.numel() * scratch.element_size(), stream_handle(stream)),
           "fused det")

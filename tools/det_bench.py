@@ -62,7 +62,7 @@ def main():
         n = min(args.nodes, pl.node_count)
         dp = st.dp
         c = st.ctx(0)
-        t = timed(lambda: native.eval_det_fused(c, st.work, dp.outer, dp.E, pl.shape[-1], dp.ids, pl.r, 0, n,
+        t = timed(lambda: native.eval_det_fused(c, st.work, dp.outer, dp.E, dp.k, pl.shape[-1], dp.ids, pl.r, 0, n,
                                                 st.det[:n], st.scratch), args.reps)
         W = (40 ** 3 - 40) // 3
         out["fused_c5"] = {"nodes": n, "s": t, "dets_per_s": n / t, "gupd_per_s": n * W / t / 1e9}
