@@ -34,7 +34,7 @@ namespace pdb {
 constexpr int GJ_B = 8;
 
 #ifndef PDB_GJ_MINB
-#define PDB_GJ_MINB 3   // resident CTAs per SM the register budget is sized for
+#define PDB_GJ_MINB 2   // resident 256-thread CTAs per SM the register budget is sized for
 #endif
 
 struct GjGeom {
@@ -46,11 +46,11 @@ struct GjGeom {
   int U;    // fused DFT-8 fill: distinct u per iteration (M = 8U); 0 = off
 };
 
-__host__ __device__ inline int gj_row_stride(int RP) {
-  int S = RP + 4;
-  while (((S >> 2) & 1) == 0) S += 4;
-  return S;
-}
+#ifndef PDB_GJ_ROWPAD
+#define PDB_GJ_ROWPAD 0   // extra words per matrix row (0: densest packing, most resident matrices)
+#endif
+
+__host__ __device__ inline int gj_row_stride(int RP) { return RP + PDB_GJ_ROWPAD; }
 
 // REDC of a <= 9-product accumulator, canonical: two conditional subtractions.
 __device__ __forceinline__ uint32_t gj_red(uint64_t acc, const Mod32& m) {
@@ -108,7 +108,7 @@ __device__ __forceinline__ void gj_fill(const StagedSrc& src, uint32_t* mats, co
     uint32_t* dst = mats + (size_t)slot * g.MS;
     GjPos pi(threadIdx.x / M, blockDim.x / M, RP);
     for (; pi.i < RP; pi.next()) {
-      if (pi.i < r && pi.j < r) gj_cp_async4(dst + pi.i * S + pi.j, col + (int64_t)ids[pi.i * r + pi.j] * src.stride);
+      if (pi.i < r && pi.j < r) gj_cp_async4(dst + pi.i * S + pi.j, col + (int64_t)__ldg(ids + pi.i * r + pi.j) * src.stride);
       else dst[pi.i * S + pi.j] = pi.i == pi.j ? one : 0u;
     }
   }
@@ -124,7 +124,7 @@ __device__ __forceinline__ void gj_fill(const FusedSrc& src, uint32_t* mats, con
   uint32_t* dst = mats + (size_t)slot * g.MS;
   GjPos pi(threadIdx.x / M, blockDim.x / M, RP);
   for (; pi.i < RP; pi.next())
-    dst[pi.i * S + pi.j] = (pi.i < r && pi.j < r) ? src.get(ids[pi.i * r + pi.j], node_lo + n)
+    dst[pi.i * S + pi.j] = (pi.i < r && pi.j < r) ? src.get(__ldg(ids + pi.i * r + pi.j), node_lo + n)
                                                   : (pi.i == pi.j ? one : 0u);
 }
 
@@ -208,8 +208,8 @@ __device__ __forceinline__ void gj_fill_dft8_e(const FusedSrc& src, uint32_t* ma
     const bool hb = ib < RP;
     if (hb) pi.next();
     const bool ra = ia < r && ja < r, rb = hb && ib < r && jb < r;
-    const uint32_t* pa = slab + (ra ? ids[ia * r + ja] : 0);
-    const uint32_t* pb = slab + (rb ? ids[ib * r + jb] : 0);
+    const uint32_t* pa = slab + (ra ? __ldg(ids + ia * r + ja) : 0);
+    const uint32_t* pb = slab + (rb ? __ldg(ids + ib * r + jb) : 0);
     uint32_t ca[E], cb[E];
 #pragma unroll
     for (int l = 0; l < E; ++l) { ca[l] = __ldg(pa + (int64_t)l * k); cb[l] = __ldg(pb + (int64_t)l * k); }
@@ -332,10 +332,57 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
     const int passes = (t + LPM - 1) / LPM;
     return (float)t / (float)(passes * LPM);
   };
-  if (util(2, 8) >= 0.7f) gj_tpass<2, 8, LPM>(A, S, K, mrem, cR, l, m);
+  // 2x8 tiles need ~70 registers: only when fewer than 4 CTAs share an SM
+  if (PDB_GJ_MINB < 4 && util(2, 8) >= 0.7f) gj_tpass<2, 8, LPM>(A, S, K, mrem, cR, l, m);
   else if (util(2, 4) >= 0.7f) gj_tpass<2, 4, LPM>(A, S, K, mrem, cR, l, m);
   else if (util(1, 4) >= 0.7f) gj_tpass<1, 4, LPM>(A, S, K, mrem, cR, l, m);
   else gj_tpass<1, 2, LPM>(A, S, K, mrem, cR, l, m);
+}
+
+// ---- M pass: negM[j][c] = sum_q negX[j][q] A12[q][c], in place in pivot rows K..K+7 ----
+// Items (column c, group of RPI rows j); the lanes sharing a column read it
+// completely before any of them overwrites it.
+template <int RPI, int LPM>
+__device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S, int K, int mrem, int l,
+                                         unsigned omask, const Mod32& m) {
+  constexpr int G = GJ_B / RPI;
+  const int items = mrem * G;
+  for (int w0 = 0; w0 < items; w0 += LPM) {
+    const int w = w0 + l;
+    uint32_t res[RPI];
+    int c = 0, jg = 0;
+    const bool act = w < items;
+    if (act) {
+      jg = w / mrem;
+      c = K + GJ_B + (w - jg * mrem);
+      uint32_t a[GJ_B];
+#pragma unroll
+      for (int q = 0; q < GJ_B; ++q) a[q] = A[(K + q) * S + c];
+#pragma unroll
+      for (int t = 0; t < RPI; ++t) {
+        uint32_t x[GJ_B];
+        gj_ld<GJ_B>(NX + (jg * RPI + t) * GJ_B, x);
+        uint64_t acc = mad_wide(x[0], a[0], 0ull);
+#pragma unroll
+        for (int q = 1; q < GJ_B; ++q) acc = mad_wide(x[q], a[q], acc);
+        res[t] = gj_red(acc, m);
+      }
+    }
+    if (G > 1) __syncwarp(omask);
+    if (act) {
+#pragma unroll
+      for (int t = 0; t < RPI; ++t) A[(K + jg * RPI + t) * S + c] = res[t];
+    }
+  }
+}
+
+template <int LPM>
+__device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, int S, int K, int mrem, int l,
+                                             unsigned omask, const Mod32& m) {
+  if (mrem * 8 <= LPM) gj_mpass<1, LPM>(A, NX, S, K, mrem, l, omask, m);
+  else if (mrem * 4 <= LPM) gj_mpass<2, LPM>(A, NX, S, K, mrem, l, omask, m);
+  else if (mrem * 2 <= LPM) gj_mpass<4, LPM>(A, NX, S, K, mrem, l, omask, m);
+  else gj_mpass<8, LPM>(A, NX, S, K, mrem, l, omask, m);
 }
 
 // ---- the kernel ------------------------------------------------------------------------------
@@ -349,8 +396,8 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
   constexpr int EPL = 8 / LPR;   // pivot-block elements per lane
   extern __shared__ __align__(16) uint32_t smem[];
   const int r = g.r, RP = g.RP, S = g.S;
-  int32_t* ids = reinterpret_cast<int32_t*>(smem);
-  uint32_t* mats = smem + ((r * r + 3) & ~3);
+  const int32_t* ids = ids_g;     // read through L1 by the fills
+  uint32_t* mats = smem;
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPM, l = lane % LPM;
   const unsigned omask = (LPM == 32 ? 0xffffffffu : ((1u << LPM) - 1u)) << (grp * LPM);
@@ -360,7 +407,6 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
   const uint32_t p = m.p, one = m.r1;
   const int pj = l / LPR, pc = EPL * (l % LPR);   // my pivot-block row / first column
 
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) ids[e] = ids_g[e];
   const int64_t iters = DFT8 ? (nodes / g.M) : (nodes + g.M - 1) / g.M;
 
   for (int64_t it = blockIdx.x; it < iters; it += gridDim.x) {
@@ -420,47 +466,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       }
       __syncwarp(omask);
       // ---------------- M: negM = negX * A12, in place in the pivot rows ----------------
-      {
-        int G = 1;
-        while (G < GJ_B && mrem * G * 2 <= LPM) G *= 2;
-        const int rpi = GJ_B / G;
-        const int items = mrem * G;
-        for (int w0 = 0; w0 < items; w0 += LPM) {
-          const int w = w0 + l;
-          uint32_t res[GJ_B];
-          int c = 0, jg = 0;
-          if (w < items) {
-            jg = w / mrem;
-            c = K + GJ_B + (w - jg * mrem);
-            uint32_t a[GJ_B];
-#pragma unroll
-            for (int q = 0; q < GJ_B; ++q) a[q] = A[(K + q) * S + c];
-#pragma unroll
-            for (int t = 0; t < GJ_B; ++t) {
-              if (t < rpi) {
-                const uint32_t* xr = NX + (jg * rpi + t) * GJ_B;
-                const uint4 x0 = *reinterpret_cast<const uint4*>(xr);
-                const uint4 x1 = *reinterpret_cast<const uint4*>(xr + 4);
-                uint64_t acc = mad_wide(x0.x, a[0], 0ull);
-                acc = mad_wide(x0.y, a[1], acc);
-                acc = mad_wide(x0.z, a[2], acc);
-                acc = mad_wide(x0.w, a[3], acc);
-                acc = mad_wide(x1.x, a[4], acc);
-                acc = mad_wide(x1.y, a[5], acc);
-                acc = mad_wide(x1.z, a[6], acc);
-                acc = mad_wide(x1.w, a[7], acc);
-                res[t] = gj_red(acc, m);
-              }
-            }
-          }
-          __syncwarp(omask);
-          if (w < items) {
-#pragma unroll
-            for (int t = 0; t < GJ_B; ++t)
-              if (t < rpi) A[(K + jg * rpi + t) * S + c] = res[t];
-          }
-        }
-      }
+      gj_mpass_any<LPM>(A, NX, S, K, mrem, l, omask, m);
       __syncwarp(omask);
       // ---------------- T: trailing rows ----------------
       gj_tpass_any<LPM>(A, S, K, mrem, cR, l, m);
@@ -526,17 +532,17 @@ inline GjGeom gj_geom(int r, int warps, int lpm, bool dft8) {
 }
 
 inline size_t gj_smem(const GjGeom& g) {
-  return sizeof(uint32_t) * ((size_t)((g.r * g.r + 3) & ~3) + (size_t)g.M * g.MS);
+  return sizeof(uint32_t) * (size_t)g.M * g.MS;
 }
 
-// lanes per matrix: a full warp once the trailing blocks are large enough
+// lanes per matrix (measured on B200, profiles/README_r01.md: 16 beats 32 and 8 at r = 40)
 inline int gj_lpm(int r) {
   static const char* env = getenv("PDB_GJ_LPM");
-  if (env) {
+  if (env && *env) {
     const int v = atoi(env);
     return v == 8 || v == 16 ? v : 32;
   }
-  return r > 24 ? 32 : (r > 16 ? 16 : 8);
+  return r > 16 ? 16 : 8;
 }
 
 // warps per CTA: DFT-8 needs M % 8 == 0; otherwise as many resident matrices as fit

@@ -16,7 +16,7 @@
 
 struct Mod32 {
   uint32_t p;        // the prime
-  uint32_t pinv;     // -p^-1 mod 2^32 (Montgomery)
+  uint32_t qinv;     // p^-1 mod 2^32 (Montgomery, subtractive form)
   uint32_t mu;       // floor(2^32 / p)   (canon32)
   uint32_t r2;       // 2^64 mod p        (to_mont)
   uint32_t r1;       // 2^32 mod p
@@ -96,13 +96,14 @@ PDB_HD uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c) {
 #endif
 }
 
-// Montgomery reduction: returns v == acc * 2^-32 (mod p) with v < 2^32,
-// valid whenever acc < (2^32 - p - 1) * 2^32 (e.g. <= 12 products of residues
-// when p < 2^30).
+// Montgomery reduction, subtractive form: with mq = lo(acc) * p^-1 mod 2^32,
+// lo(mq * p) == lo(acc), so acc - mq*p = (hi(acc) - hi(mq*p)) * 2^32 exactly and
+//   v = hi(acc) + p - hi(mq*p) == acc * 2^-32 (mod p),  0 < v <= hi(acc) + p.
+// Three instructions (IMAD, IMAD.HI, IADD3); valid whenever hi(acc) + p < 2^32,
+// e.g. up to 12 products of residues when p < 2^30.
 PDB_HD uint32_t redc(uint64_t acc, const Mod32& m) {
-  uint32_t mq = (uint32_t)acc * m.pinv;
-  uint64_t s = (uint64_t)mq * m.p + acc;  // exact: no 64-bit overflow under the bound
-  return (uint32_t)(s >> 32);
+  const uint32_t mq = (uint32_t)acc * m.qinv;
+  return (uint32_t)(acc >> 32) + m.p - umulhi32(mq, m.p);
 }
 
 // Any 32-bit v -> [0, p).
@@ -149,7 +150,7 @@ inline Mod32 make_mod32(uint32_t p) {
   m.p = p;
   uint32_t inv = 1;  // Newton iteration for p^-1 mod 2^32
   for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
-  m.pinv = 0u - inv;
+  m.qinv = inv;
   m.mu = (uint32_t)((((uint64_t)1) << 32) / p);
   m.r1 = (uint32_t)((((uint64_t)1) << 32) % p);
   m.r2 = (uint32_t)(((unsigned __int128)1 << 64) % p);

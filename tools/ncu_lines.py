@@ -73,6 +73,8 @@ def main():
     base = int(rows[0]["Address"], 16)
     agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0])
     tot = [0.0, 0.0, 0.0]
+    reasons = [c for c in rows[0] if c.startswith("stall_") and "Not Issued" not in c]
+    why = collections.defaultdict(collections.Counter)
     for r in rows:
         off = int(r["Address"], 16) - base
         loc = lmap.get(off, ("?", 0))
@@ -81,12 +83,15 @@ def main():
         for i in range(3):
             agg[loc][i] += v[i]
             tot[i] += v[i]
+        for c in reasons:
+            why[loc][c[6:]] += num(r[c])
     print("kernel:", kernel)
     print("function:", fn, " sass rows:", n, " mapped:", len(lmap))
     print("%-28s %10s %8s %8s" % ("file:line", "thr-inst%", "stall%", "warp-inst%"))
     for loc, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-        print("%-28s %9.2f%% %7.2f%% %8.2f%%" % ("%s:%d" % loc, 100 * v[0] / tot[0], 100 * v[1] / max(tot[1], 1),
-                                                100 * v[2] / tot[2]))
+        top3 = ", ".join("%s %.0f%%" % (k, 100 * n / max(v[1], 1)) for k, n in why[loc].most_common(3))
+        print("%-28s %9.2f%% %7.2f%% %8.2f%%   %s" % ("%s:%d" % loc, 100 * v[0] / tot[0], 100 * v[1] / max(tot[1], 1),
+                                                     100 * v[2] / tot[2], top3))
 
 
 if __name__ == "__main__":
