@@ -85,12 +85,15 @@ PDB_HD uint32_t mul_mod(uint32_t a, uint32_t b, const Mod32& m) {
   return csub((uint32_t)r, m.p);
 }
 
-// c + a*b as one IMAD.WIDE.U32 (64-bit accumulate of a 32x32 product).
+// c + a*b as one IMAD.WIDE.U32 (64-bit accumulate of a 32x32 product).  Written
+// as a carry chain on the 32-bit halves: ptxas fuses mad.lo.cc + madc.hi into a
+// single accumulating IMAD.WIDE.U32, whereas mad.wide.u32 with a 64-bit addend
+// is split into IMAD.WIDE + IADD3 + IADD3.X (tools/microbench/mac.cu).
 PDB_HD uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c) {
 #ifdef __CUDA_ARCH__
-  uint64_t d;
-  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
-  return d;
+  uint32_t lo = (uint32_t)c, hi = (uint32_t)(c >> 32);
+  asm("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.u32 %1, %2, %3, %1;" : "+r"(lo), "+r"(hi) : "r"(a), "r"(b));
+  return ((uint64_t)hi << 32) | lo;
 #else
   return c + (uint64_t)a * b;
 #endif
