@@ -28,6 +28,7 @@
 // applies the reference's first-nonzero pivoting (determinant.py:136-169).
 #pragma once
 #include "pdb_internal.cuh"
+#include "dft8.cuh"
 
 namespace pdb {
 
@@ -128,45 +129,6 @@ __device__ __forceinline__ void gj_fill(const FusedSrc& src, uint32_t* mats, con
                                                   : (pi.i == pi.j ? one : 0u);
 }
 
-// Radix-2 butterfly (x, y) -> (x + y, x - y); ZERO: y is known to be 0.
-template <bool ZERO>
-__device__ __forceinline__ void gj_bf(uint32_t& x, uint32_t& y, uint32_t p) {
-  if constexpr (ZERO) {
-    y = x;
-  } else {
-    const uint32_t t = y;
-    y = sub_mod(x, t, p);
-    x = add_mod(x, t, p);
-  }
-}
-
-// X[v] = sum_{l<E} c_l w^(u l) w8^(l v), v < 8: twist, then an 8-point DIT
-// transform whose first stage is trivial for the coefficient slots >= E.
-template <int E>
-__device__ __forceinline__ void gj_dft8(const uint32_t (&c)[E], const uint32_t* tw, const uint32_t* tws,
-                                        const uint32_t (&w)[4], const uint32_t (&ws)[4], uint32_t p,
-                                        uint32_t (&x)[8]) {
-  uint32_t q[8];
-  q[0] = c[0];
-#pragma unroll
-  for (int l = 1; l < 8; ++l) q[l] = l < E ? shoup_mul(c[l < E ? l : 0], tw[l], tws[l], p) : 0u;
-  // bit-reversed order
-  x[0] = q[0]; x[1] = q[4]; x[2] = q[2]; x[3] = q[6]; x[4] = q[1]; x[5] = q[5]; x[6] = q[3]; x[7] = q[7];
-  gj_bf<(4 >= E)>(x[0], x[1], p);
-  gj_bf<(6 >= E)>(x[2], x[3], p);
-  gj_bf<(5 >= E)>(x[4], x[5], p);
-  gj_bf<(7 >= E)>(x[6], x[7], p);
-  uint32_t t;
-  gj_bf<false>(x[0], x[2], p);
-  t = shoup_mul(x[3], w[2], ws[2], p); x[3] = t; gj_bf<false>(x[1], x[3], p);
-  gj_bf<false>(x[4], x[6], p);
-  t = shoup_mul(x[7], w[2], ws[2], p); x[7] = t; gj_bf<false>(x[5], x[7], p);
-  gj_bf<false>(x[0], x[4], p);
-  t = shoup_mul(x[5], w[1], ws[1], p); x[5] = t; gj_bf<false>(x[1], x[5], p);
-  t = shoup_mul(x[6], w[2], ws[2], p); x[6] = t; gj_bf<false>(x[2], x[6], p);
-  t = shoup_mul(x[7], w[3], ws[3], p); x[7] = t; gj_bf<false>(x[3], x[7], p);
-}
-
 // 8 nodes per thread: f(o*NL + u + (NL/8) v) = sum_l (T_l w^(u l)) w8^(l v) for
 // the slot v*U + uu.  The coefficients of one outer index o are the slab
 // part[o][l][e] (entries innermost): consecutive threads read consecutive
@@ -239,8 +201,75 @@ __device__ __forceinline__ void gj_fill_dft8_e(const FusedSrc& src, uint32_t* ma
   }
 }
 
+// Dense case (entry_ids[p] == p, no padding: the C3/C5 shape): position p is
+// entry p and smem word p of its matrix, so addressing is affine and four
+// positions (4E coalesced loads) are kept in flight per thread.
+template <int E>
+__device__ __forceinline__ void gj_fill_dft8_dense(const FusedSrc& src, uint32_t* mats, const GjGeom& g,
+                                                   int64_t it, int64_t node_lo) {
+  const int U = g.U, NL = src.NL, k = src.k, n = g.r * g.r;
+  const uint32_t p = src.p;
+  const int per_o = NL / (8 * U);
+  const int64_t o = (node_lo / NL) + it / per_o;
+  const int ublk = (int)(it % per_o);
+  const int step8 = NL / 8;
+  uint32_t w[4], ws[4];
+#pragma unroll
+  for (int v = 1; v < 4; ++v) { w[v] = __ldg(src.xs + v * step8); ws[v] = __ldg(src.xss + v * step8); }
+  w[0] = ws[0] = 0;
+  const int uu = threadIdx.x % U;
+  uint32_t tw[8], tws[8];
+  {
+    const int u = ublk * U + uu;
+    int kk = 0;
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      if (l < E) { tw[l] = __ldg(src.xs + kk); tws[l] = __ldg(src.xss + kk); }
+      else { tw[l] = tws[l] = 0; }
+      kk += u;
+      if (kk >= NL) kk -= NL;
+    }
+  }
+  const int ms = U * g.MS;
+  uint32_t* base = mats + uu * g.MS;
+  const uint32_t* slab = src.part + o * (int64_t)E * k;
+  const int step = blockDim.x / U;
+  constexpr int F = 4;   // positions in flight
+  for (int p0 = threadIdx.x / U; p0 < n; p0 += F * step) {
+    uint32_t c[F][E];
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      const int q = p0 + f * step < n ? p0 + f * step : p0;
+#pragma unroll
+      for (int l = 0; l < E; ++l) c[f][l] = __ldg(slab + l * k + q);
+    }
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      const int q = p0 + f * step;
+      if (q < n) {
+        uint32_t x[8];
+        gj_dft8<E>(c[f], tw, tws, w, ws, p, x);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) base[v * ms + q] = x[v];
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void gj_fill_dft8(const FusedSrc& src, uint32_t* mats, const GjGeom& g, const int32_t* ids,
-                                             int64_t it, int64_t node_lo, uint32_t one) {
+                                             int64_t it, int64_t node_lo, uint32_t one, bool dense) {
+  if (dense) {
+    switch (src.E) {
+      case 1: gj_fill_dft8_dense<1>(src, mats, g, it, node_lo); return;
+      case 2: gj_fill_dft8_dense<2>(src, mats, g, it, node_lo); return;
+      case 3: gj_fill_dft8_dense<3>(src, mats, g, it, node_lo); return;
+      case 4: gj_fill_dft8_dense<4>(src, mats, g, it, node_lo); return;
+      case 5: gj_fill_dft8_dense<5>(src, mats, g, it, node_lo); return;
+      case 6: gj_fill_dft8_dense<6>(src, mats, g, it, node_lo); return;
+      case 7: gj_fill_dft8_dense<7>(src, mats, g, it, node_lo); return;
+      default: gj_fill_dft8_dense<8>(src, mats, g, it, node_lo); return;
+    }
+  }
   switch (src.E) {
     case 1: gj_fill_dft8_e<1>(src, mats, g, ids, it, node_lo, one); break;
     case 2: gj_fill_dft8_e<2>(src, mats, g, ids, it, node_lo, one); break;
@@ -340,38 +369,50 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
 }
 
 // ---- M pass: negM[j][c] = sum_q negX[j][q] A12[q][c], in place in pivot rows K..K+7 ----
-// Items (column c, group of RPI rows j); the lanes sharing a column read it
-// completely before any of them overwrites it.
-template <int RPI, int LPM>
+// Register tiles of RPI rows x TC columns per lane: one item reads the 8 x TC
+// block of A12 and RPI rows of negX (16 B loads) for RPI*TC*8 MACs.  Items are
+// numbered column-group major, so the lanes sharing a column group work in the
+// same pass; they read it completely before any of them overwrites it.
+template <int RPI, int TC, int LPM>
 __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S, int K, int mrem, int l,
                                          unsigned omask, const Mod32& m) {
-  constexpr int G = GJ_B / RPI;
-  const int items = mrem * G;
+  constexpr int NRG = GJ_B / RPI;
+  const int items = (mrem / TC) * NRG;
   for (int w0 = 0; w0 < items; w0 += LPM) {
     const int w = w0 + l;
-    uint32_t res[RPI];
-    int c = 0, jg = 0;
     const bool act = w < items;
+    const int cg = w / NRG, rg = w - (w / NRG) * NRG;
+    const int c = K + GJ_B + TC * cg;
+    uint32_t res[RPI][TC];
     if (act) {
-      jg = w / mrem;
-      c = K + GJ_B + (w - jg * mrem);
-      uint32_t a[GJ_B];
+      uint64_t acc[RPI][TC];
 #pragma unroll
-      for (int q = 0; q < GJ_B; ++q) a[q] = A[(K + q) * S + c];
+      for (int q = 0; q < GJ_B; ++q) {
+        uint32_t a[TC];
+        gj_ld<TC>(A + (K + q) * S + c, a);
+        if (q == 0) {
 #pragma unroll
-      for (int t = 0; t < RPI; ++t) {
-        uint32_t x[GJ_B];
-        gj_ld<GJ_B>(NX + (jg * RPI + t) * GJ_B, x);
-        uint64_t acc = mad_wide(x[0], a[0], 0ull);
+          for (int t = 0; t < RPI; ++t)
 #pragma unroll
-        for (int q = 1; q < GJ_B; ++q) acc = mad_wide(x[q], a[q], acc);
-        res[t] = gj_red(acc, m);
+            for (int b = 0; b < TC; ++b) acc[t][b] = mad_wide(NX[(rg * RPI + t) * GJ_B], a[b], 0ull);
+        } else {
+#pragma unroll
+          for (int t = 0; t < RPI; ++t) {
+            const uint32_t x = NX[(rg * RPI + t) * GJ_B + q];
+#pragma unroll
+            for (int b = 0; b < TC; ++b) acc[t][b] = mad_wide(x, a[b], acc[t][b]);
+          }
+        }
       }
+#pragma unroll
+      for (int t = 0; t < RPI; ++t)
+#pragma unroll
+        for (int b = 0; b < TC; ++b) res[t][b] = gj_red(acc[t][b], m);
     }
-    if (G > 1) __syncwarp(omask);
+    if (NRG > 1) __syncwarp(omask);
     if (act) {
 #pragma unroll
-      for (int t = 0; t < RPI; ++t) A[(K + jg * RPI + t) * S + c] = res[t];
+      for (int t = 0; t < RPI; ++t) gj_st<TC>(A + (K + rg * RPI + t) * S + c, res[t]);
     }
   }
 }
@@ -379,10 +420,16 @@ __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S,
 template <int LPM>
 __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, int S, int K, int mrem, int l,
                                              unsigned omask, const Mod32& m) {
-  if (mrem * 8 <= LPM) gj_mpass<1, LPM>(A, NX, S, K, mrem, l, omask, m);
-  else if (mrem * 4 <= LPM) gj_mpass<2, LPM>(A, NX, S, K, mrem, l, omask, m);
-  else if (mrem * 2 <= LPM) gj_mpass<4, LPM>(A, NX, S, K, mrem, l, omask, m);
-  else gj_mpass<8, LPM>(A, NX, S, K, mrem, l, omask, m);
+  auto util = [&](int rpi, int tc) {
+    const int t = (mrem / tc) * (GJ_B / rpi);
+    return (float)t / (float)(((t + LPM - 1) / LPM) * LPM);
+  };
+  if (util(4, 4) >= 0.74f) gj_mpass<4, 4, LPM>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(2, 4) >= 0.74f) gj_mpass<2, 4, LPM>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(4, 2) >= 0.74f) gj_mpass<4, 2, LPM>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(1, 4) >= 0.74f) gj_mpass<1, 4, LPM>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(2, 2) >= 0.74f) gj_mpass<2, 2, LPM>(A, NX, S, K, mrem, l, omask, m);
+  else gj_mpass<1, 2, LPM>(A, NX, S, K, mrem, l, omask, m);
 }
 
 // ---- the kernel ------------------------------------------------------------------------------
@@ -408,10 +455,16 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
   const int pj = l / LPR, pc = EPL * (l % LPR);   // my pivot-block row / first column
 
   const int64_t iters = DFT8 ? (nodes / g.M) : (nodes + g.M - 1) / g.M;
+  bool dense = false;
+  if constexpr (DFT8) {
+    bool id = g.RP == r && g.S == r;
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) id = id && __ldg(ids + e) == e;
+    dense = __syncthreads_and(id) != 0;
+  }
 
   for (int64_t it = blockIdx.x; it < iters; it += gridDim.x) {
     __syncthreads();
-    if constexpr (DFT8) gj_fill_dft8(src, mats, g, ids, it, node_lo, one);
+    if constexpr (DFT8) gj_fill_dft8(src, mats, g, ids, it, node_lo, one, dense);
     else gj_fill(src, mats, g, ids, it, node_lo, nodes, one);
     __syncthreads();
     int64_t node;
@@ -448,11 +501,17 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
           const uint32_t nv = gj_red2(mad_wide(z, diag ? 0u : v[k], mad_wide(nt, diag ? lam : prow[k], 0ull)), m);
           v[k] = pj != s ? nv : (diag ? lam : v[k]);
         }
-        if (s >= 1 && s <= 6) den = gj_mont(den, lam, m);
         if (s == GJ_B - 1) z7 = z;
         lam = gj_mont(lam, z, m);
       }
       if (zero) { ok = false; break; }
+      {
+        // den *= lambda_1 ... lambda_6: row pj holds lambda_pj = zl; product over the rows
+        uint32_t f = (pj >= 1 && pj <= 6) ? zl : one;
+#pragma unroll
+        for (int d = LPR; d < LPM; d <<= 1) f = gj_mont(f, __shfl_xor_sync(omask, f, d, LPM), m);
+        den = gj_mont(den, f, m);
+      }
       num = gj_mont(num, z7, m);
       if (mrem == 0) break;
       const uint32_t cR = lam;   // c = prod z_s

@@ -14,7 +14,9 @@
 // zero (outside the coefficient box on not-yet-transformed axes) are skipped
 // ("pruning"): for an entry with (d+1)^vn coefficients only the first pass
 // touches (d+1)^(vn-1) lines per entry.
+#include <cstdlib>
 #include "pdb_internal.cuh"
+#include "dft8.cuh"
 
 namespace pdb {
 
@@ -153,6 +155,60 @@ __global__ void ntt_stage_global(uint32_t* __restrict__ data, AxisGeom g, int N,
   }
 }
 
+// ---- sparse forward axis: input nonzero only on rows j < E <= 8 ------------
+// out[k] = sum_{j<E} x_j w^(jk) for every k = u + (N/8) v: the E input rows of
+// a tile of TI inner indices are staged in shared memory (every writer of
+// rows < E is in this CTA), then each thread evaluates 8 outputs of one
+// (u, t) by a twisted 8-point DFT.  Reads E/N of the axis instead of all of
+// it and does ~(E + 4)/8 mul-mods per output instead of log2(N)/2.  The
+// entries' coefficient boxes make this the common case of forward passes.
+template <int E>
+__global__ void __launch_bounds__(256)
+ntt_axis_sparse(uint32_t* __restrict__ data, AxisGeom g, int N, int TI, const uint32_t* __restrict__ full,
+                const uint32_t* __restrict__ fulls, uint32_t p) {
+  __shared__ uint32_t xs[E * 32];
+  const int N8 = N / 8;
+  const int64_t tchunks = (g.inner + TI - 1) / TI;
+  const int64_t ntiles = g.active_outer * tchunks;
+  uint32_t w[4], ws[4];
+  w[0] = ws[0] = 0;
+#pragma unroll
+  for (int v = 1; v < 4; ++v) { w[v] = __ldg(full + v * N8); ws[v] = __ldg(fulls + v * N8); }
+  const int t = threadIdx.x % TI;
+  const int ug = threadIdx.x / TI, ugs = blockDim.x / TI;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t oc = tile / tchunks;
+    const int64_t t0 = (tile - oc * tchunks) * TI;
+    const int64_t base = outer_offset(oc, g) * (int64_t)N * g.inner + t0;
+    const bool live = t0 + t < g.inner;
+    __syncthreads();
+    for (int w2 = threadIdx.x; w2 < E * TI; w2 += blockDim.x) {
+      const int j = w2 / TI, tt = w2 - (w2 / TI) * TI;
+      xs[j * TI + tt] = t0 + tt < g.inner ? data[base + (int64_t)j * g.inner + tt] : 0u;
+    }
+    __syncthreads();
+    if (live && ug < ugs) {
+      uint32_t c[E];
+#pragma unroll
+      for (int j = 0; j < E; ++j) c[j] = xs[j * TI + t];
+      for (int u = ug; u < N8; u += ugs) {
+        uint32_t tw[8], tws[8];
+        int kk = 0;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          if (l < E) { tw[l] = __ldg(full + kk); tws[l] = __ldg(fulls + kk); }
+          else { tw[l] = tws[l] = 0; }
+          kk += u;
+        }
+        uint32_t x[8];
+        gj_dft8<E>(c, tw, tws, w, ws, p, x);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) data[base + (int64_t)(u + v * N8) * g.inner + t] = x[v];
+      }
+    }
+  }
+}
+
 // Transform one axis of `batch` tensors of shape dims[0..nd) in place.
 // ext (may be null) gives, per dim, how many leading indices can be nonzero
 // on the dims before `axis` (lines outside that box are skipped).
@@ -176,6 +232,24 @@ int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t
   for (int d = 0; d < g.nbox; ++d) g.active_outer *= g.box_ext[d];
   if (g.active_outer == 0 || g.inner == 0) return 0;
   const int logN = 31 - __builtin_clz((unsigned)N);
+  const int64_t E = ext ? ext[axis] : N;
+  if (!inverse && E >= 1 && E <= 8 && N >= 16 && !getenv("PDB_NTT_DENSE")) {
+    // the input is nonzero only on rows < E of this axis: evaluate, don't transform
+    const int TI = (int)(g.inner < 32 ? g.inner : 32);
+    const int threads = (256 / TI) * TI;
+    const int64_t tiles = g.active_outer * ((g.inner + TI - 1) / TI);
+    const int grid = (int)(tiles < (int64_t)ctx->sms * 16 ? tiles : (int64_t)ctx->sms * 16);
+    const uint32_t p = (uint32_t)ctx->p;
+    switch (E) {
+#define PDB_SPARSE(EE) case EE: ntt_axis_sparse<EE><<<grid, threads, 0, st>>>(data, g, N, TI, T->full, T->full_s, p); break;
+      PDB_SPARSE(1) PDB_SPARSE(2) PDB_SPARSE(3) PDB_SPARSE(4)
+      PDB_SPARSE(5) PDB_SPARSE(6) PDB_SPARSE(7) PDB_SPARSE(8)
+#undef PDB_SPARSE
+      default: break;
+    }
+    count_launch();
+    return check_launch("ntt_axis_sparse");
+  }
   const uint32_t* tw = inverse ? T->inv : T->fwd;
   const uint32_t* tws = inverse ? T->inv_s : T->fwd_s;
   if (N <= PDB_SMEM_NTT_MAX) {

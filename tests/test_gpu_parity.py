@@ -76,6 +76,30 @@ def test_ntt_long_axes_global_path(cuda):
     assert got.tolist() == O.ntt_multi(x, (2, 16384), spec.p, spec.omega, spec.q).tolist()
 
 
+@pytest.mark.parametrize("shape", [(16,), (64, 32), (16, 8, 256), (256, 4, 2)])
+def test_ntt_sparse_axes_equal_dense(cuda, shape):
+    """Forward passes over axes whose input is nonzero only on the first E <= 8
+    rows take the evaluation kernel; it must equal the full transform."""
+    import torch
+    from paper_2010_12117_b200 import native
+    spec = find_fourier_primes(8, 1, start=10**9, min_count=1)[0]
+    ctx = native.prime_context(spec)
+    rng = np.random.default_rng(len(shape))
+    for E in range(1, 9):
+        ext = [min(E + a, n) for a, n in enumerate(shape)]
+        x = np.zeros(shape, dtype=np.int64)
+        box = tuple(slice(0, e) for e in ext)
+        x[box] = rng.integers(0, spec.p, [e for e in ext])
+        batch = 3
+        data = torch.tensor(np.concatenate([x.ravel()] * batch), dtype=torch.int64).to(torch.int32).cuda()
+        ref = data.clone()
+        native.ntt_multi(ctx, data, batch, shape, ext, range(len(shape)), False)
+        native.ntt_multi(ctx, ref, batch, shape, None, range(len(shape)), False)
+        assert torch.equal(data, ref), (shape, E)
+        want = O.ntt_multi(x.ravel(), shape, spec.p, spec.omega, spec.q)
+        assert data[: x.size].cpu().numpy().astype(np.int64).tolist() == want.tolist()
+
+
 def test_ntt_small_naive_and_errors(cuda):
     spec = find_fourier_primes(10, 1, start=10**6, min_count=1)[0]
     table = TwiddleTable(spec)
