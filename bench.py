@@ -310,6 +310,15 @@ def run_ours(args):
     W = (r ** 3 - r) // 3
     achieved = W * nodes * args.steps / (det_ms / 1e3)
     hbm, hbm_kind = measured_peaks()
+    from paper_2010_12117_b200.executor import FUSED_CHUNK
+    launch_nodes = min(nodes, FUSED_CHUNK)
+    traffic = traffic_note = None
+    tpath = ROOT / "profiles" / "ncu" / "det_traffic_r01.json"
+    if tpath.exists() and args.config == "c5":
+        t = json.loads(tpath.read_text())
+        traffic = t["dram_bytes_per_node"] * launch_nodes
+        traffic_note = ("dram read+write bytes per launch of %d nodes, scaled from %s (%d-node launch)"
+                        % (launch_nodes, t["source"], t["nodes_per_launch"]))
     out = {
         "metric": "mod-p %dx%d dets/sec (%s)" % (r, r, args.config.upper()),
         "value": value, "unit": "dets/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -322,7 +331,9 @@ def run_ours(args):
                 "ms_per_step": e_ms / args.steps},
         "roofline": {"bound": "int", "kernel": "det_gj_kernel<FusedSrc> (eval + elimination)",
                      "achieved": achieved / 1e9, "peak": peak_delayed / 1e9, "unit": "Gupd/s",
-                     "frac": achieved / peak_delayed, "traffic": None,
+                     "frac": achieved / peak_delayed, "traffic": traffic, "traffic_note": traffic_note,
+                     "hbm_achieved_gbs": (traffic / launch_nodes) * nodes * args.steps / (det_ms / 1e3) / 1e9
+                     if traffic else None,
                      "peak_kind": "measured now: delayed 64-bit MAC + REDC primitive (pdb_mulmod_peak v1)",
                      "shoup_peak": peak_shoup / 1e9, "frac_vs_shoup_peak": achieved / peak_shoup,
                      "det_ms_per_step": det_ms / args.steps, "det_share": det_ms / ms,

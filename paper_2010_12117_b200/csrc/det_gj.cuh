@@ -609,7 +609,10 @@ inline GjGeom gj_pick(int r, int lpm, bool dft8) {
   const size_t budget = 227 * 1024;
   GjGeom best = gj_geom(r, 8, lpm, dft8);
   double best_score = -1;
+  static const char* wenv = getenv("PDB_GJ_WARPS");   // experiments: force warps per CTA
+  const int wforce = wenv && *wenv ? atoi(wenv) : 0;
   for (int warps = 1; warps <= 8; ++warps) {
+    if (wforce && warps != wforce) continue;
     GjGeom g = gj_geom(r, warps, lpm, dft8);
     if (dft8 && (g.M % 8)) continue;
     const size_t sm = gj_smem(g) + 1024;
