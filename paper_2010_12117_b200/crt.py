@@ -94,7 +94,14 @@ def limbs_to_ints(limbs: np.ndarray, neg: np.ndarray) -> list:
 
 
 def device_lift(residues_dev, primes, n: int, stride: int) -> list:
-    """CRT of device residue rows [P][stride] -> list of n Python ints."""
+    """CRT of device residue rows [P][stride] -> list of n Python ints.
+
+    The GPU writes |X| as u32 limbs + a sign byte per coefficient; only the
+    nonzero coefficients, trimmed to the widest limb actually used, are copied
+    back, and the native host module (_pdb_host, csrc/host_ints.cpp) builds the
+    Python ints in one C loop (reference crt.py:122-130 materialises them with
+    Python big-int Horner).
+    """
     torch = native._torch()
     P = len(primes)
     L = native.crt_limbs(P)
@@ -103,7 +110,16 @@ def device_lift(residues_dev, primes, n: int, stride: int) -> list:
     neg = torch.empty(n, dtype=torch.uint8, device=dev)
     scratch = native.scratch_tensor(native.crt_scratch_bytes(P), dev)
     native.crt_mrc(residues_dev, P, n, stride, primes, limbs, L, neg, scratch)
-    return limbs_to_ints(native.to_host_u32(limbs).reshape(n, L), neg.cpu().numpy())
+    used = limbs != 0
+    idx = used.any(dim=1).nonzero().squeeze(1)
+    cols = used.any(dim=0).nonzero()
+    width = int(cols.max().item()) + 1 if cols.numel() else 1
+    del used
+    sel = limbs.index_select(0, idx)[:, :width].contiguous()
+    sel_neg = neg.index_select(0, idx)
+    host = native.host_module()
+    return host.ints_from_limbs(sel.cpu().numpy().tobytes(), idx.cpu().numpy().tobytes(),
+                                sel_neg.cpu().numpy().tobytes(), int(n), int(width))
 
 
 def mrc_digits(residues, basis: CrtBasis) -> list:

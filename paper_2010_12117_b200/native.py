@@ -76,6 +76,22 @@ def load_library():
         return lib
 
 
+_host = None
+
+
+def host_module():
+    """The native host module (csrc/host_ints.cpp): result materialisation."""
+    global _host
+    if _host is None:
+        try:
+            from . import _pdb_host
+        except ImportError as exc:
+            raise DeviceError("_pdb_host native module not built (run __graft_entry__.build() or `make -C "
+                              "paper_2010_12117_b200/csrc`): %s" % exc) from exc
+        _host = _pdb_host
+    return _host
+
+
 def _torch():
     import torch
     if not torch.cuda.is_available():

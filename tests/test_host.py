@@ -186,3 +186,29 @@ def test_crt_host_helpers():
         signed_lift(105, 105)
     with pytest.raises(ValueError, match="duplicate"):
         build_basis([3, 5, 3])
+
+
+def test_native_ints_from_limbs_matches_python_path():
+    """_pdb_host (csrc/host_ints.cpp) builds the same Python ints as the
+    reference-style per-coefficient from_bytes path, for any limb width."""
+    from paper_2010_12117_b200 import native
+    from paper_2010_12117_b200.crt import limbs_to_ints
+    h = native.host_module()
+    rng = np.random.default_rng(7)
+    n = 5000
+    for L in (1, 2, 3, 9):
+        limbs = np.zeros((n, L), dtype=np.uint32)
+        nz = np.sort(rng.choice(n, 1700, replace=False))
+        for i in nz:
+            w = int(rng.integers(1, L + 1))
+            limbs[i, :w] = rng.integers(0, 2**32, w, dtype=np.uint32)
+        limbs[nz[:3]] = 0xFFFFFFFF                     # widest magnitudes
+        neg = rng.integers(0, 2, n).astype(np.uint8)
+        want = limbs_to_ints(limbs, neg)
+        keep = np.flatnonzero(limbs.any(axis=1))
+        got = h.ints_from_limbs(limbs[keep].tobytes(), keep.astype(np.int64).tobytes(), neg[keep].tobytes(), n, L)
+        assert got == want
+    with pytest.raises(ValueError):
+        h.ints_from_limbs(b"\0" * 8, np.zeros(1, np.int64).tobytes(), b"\0", 4, 1)
+    with pytest.raises(IndexError):
+        h.ints_from_limbs(b"\1\0\0\0", np.array([9], np.int64).tobytes(), b"\0", 4, 1)
