@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--config", default="c5", choices=["c5", "c3"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-poly", action="store_true", help="skip the end-to-end run_report timings")
     return ap.parse_args()
 
 
@@ -192,6 +193,32 @@ def run_reference(args):
                             "sample": base["sample"]},
            "e2e": {"value": value, "unit": "dets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
+
+
+def poly_e2e():
+    """Second half of the BASELINE metric: end-to-end seconds per polynomial
+    determinant through the public API (`run_report`: upload, all primes, CRT,
+    Python-int result) for C3 (reference CPU: 161.5 s with 8 workers,
+    SURVEY.md 6) and C5 (infeasible on the reference: ~11.5 days extrapolated)."""
+    from paper_2010_12117_b200 import run_report, workloads
+
+    res = []
+    for name, make, reps in (("C3", workloads.c3, 3), ("C5", workloads.c5, 1)):
+        m, cfg = make()
+        best = None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            result, timings, pl = run_report(m, cfg)
+            wall = time.perf_counter() - t0
+            if best is None or wall < best[0]:
+                best = (wall, timings, pl)
+        wall, timings, pl = best
+        res.append({"config": name, "seconds": wall, "primes": pl.prime_count, "nodes": pl.node_count,
+                    "stages_s": {"fft": timings.fft, "det": timings.det, "ifft": timings.ifft, "crt": timings.crt},
+                    "reference_cpu_s": 161.5 if name == "C3" else None,
+                    "reference_note": "SURVEY.md 6: reference run_report, 8 workers, dev container" if name == "C3"
+                    else "reference infeasible (needs >= 215 GB RAM; ~11.5 days extrapolated, SURVEY.md 6)"})
+    return res
 
 
 # -- GPU arm --------------------------------------------------------------------------------------
@@ -341,6 +368,8 @@ def run_ours(args):
         "clocks": clocks,
         "gpu_launches": launches,
     }
+    if not args.no_poly and world == 1:
+        out["poly_e2e"] = poly_e2e()
     if not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_sample(m, pl)
     print(json.dumps(out))

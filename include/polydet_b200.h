@@ -104,6 +104,31 @@ int32_t pdb_crt_mrc_u32(const uint32_t* residues, int32_t nprimes, int64_t n, in
  * variant 0 = Shoup mul-mod + sub-mod, 1 = delayed 64-bit MAC (8 per REDC). */
 int32_t pdb_mulmod_peak(uint32_t p, int32_t variant, double* updates_per_second, void* stream);
 
+/* ---- the wide path: primes 2^31 <= p < 2^62 --------------
+ * u64 twins of the entry points above for contexts created with p >= 2^31
+ * (reference object/int64 dtype paths, tensor.py:152-154).  Residues are u64;
+ * the CRT takes any mix of odd primes < 2^62 (test_crt.py:147-153).  The u32
+ * entry points reject wide contexts and vice versa. */
+int32_t pdb_prime_ctx_create_wide(uint64_t p, uint64_t omega, int32_t q, pdb_prime_ctx** out);
+int32_t pdb_ntt_multi_u64(pdb_prime_ctx* ctx, uint64_t* data, int64_t batch, int32_t ndim,
+                          const int64_t* dims, const int64_t* extents, uint32_t axis_mask,
+                          int32_t inverse, void* stream);
+int32_t pdb_reduce_scatter_u64(pdb_prime_ctx* ctx, const uint32_t* mag, const uint8_t* neg,
+                               const int64_t* pos, int64_t count, int32_t limbs, uint64_t* dst,
+                               void* stream);
+size_t pdb_det_scratch_bytes_u64(int32_t r, int64_t nodes);
+int32_t pdb_det_batch_u64(pdb_prime_ctx* ctx, const uint64_t* grids, int64_t grid_stride,
+                          const int32_t* entry_ids, int32_t r, int64_t node_lo, int64_t nodes,
+                          uint64_t* out, void* scratch, size_t scratch_bytes, void* stream);
+int32_t pdb_condense_u64(pdb_prime_ctx* ctx, const uint64_t* mat, int32_t r, uint64_t* trail_vals,
+                         int32_t* trail_cols, uint64_t* det_out, void* scratch, size_t scratch_bytes,
+                         void* stream);
+int32_t pdb_crt_limbs_u64(int32_t nprimes);
+size_t pdb_crt_scratch_bytes_u64(int32_t nprimes);
+int32_t pdb_crt_mrc_u64(const uint64_t* residues, int32_t nprimes, int64_t n, int64_t stride,
+                        const uint64_t* primes, uint32_t* limbs, int32_t L, uint8_t* neg,
+                        void* scratch, size_t scratch_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

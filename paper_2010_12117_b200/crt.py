@@ -93,6 +93,12 @@ def limbs_to_ints(limbs: np.ndarray, neg: np.ndarray) -> list:
     return out
 
 
+def wide_primes(primes) -> bool:
+    """True when the set needs the u64 kernels (some p >= 2^31); the whole set then
+    shares u64 residues."""
+    return any(native.needs_wide(int(p)) for p in primes)
+
+
 def device_lift(residues_dev, primes, n: int, stride: int) -> list:
     """CRT of device residue rows [P][stride] -> list of n Python ints.
 
@@ -104,12 +110,15 @@ def device_lift(residues_dev, primes, n: int, stride: int) -> list:
     """
     torch = native._torch()
     P = len(primes)
-    L = native.crt_limbs(P)
+    wide = wide_primes(primes)
+    if residues_dev.dtype != native.word_dtype(wide):
+        raise ValueError("residue rows must be %s for this prime set" % native.word_dtype(wide))
+    L = native.crt_limbs(P, wide)
     dev = residues_dev.device
     limbs = torch.empty((n, L), dtype=torch.int32, device=dev)
     neg = torch.empty(n, dtype=torch.uint8, device=dev)
-    scratch = native.scratch_tensor(native.crt_scratch_bytes(P), dev)
-    native.crt_mrc(residues_dev, P, n, stride, primes, limbs, L, neg, scratch)
+    scratch = native.scratch_tensor(native.crt_scratch_bytes(P, wide), dev)
+    native.crt_mrc(residues_dev, P, n, stride, primes, limbs, L, neg, scratch, wide=wide)
     used = limbs != 0
     idx = used.any(dim=1).nonzero().squeeze(1)
     cols = used.any(dim=0).nonzero()
@@ -126,8 +135,8 @@ def mrc_digits(residues, basis: CrtBasis) -> list:
     """Mixed-radix digits: X = sum digits[j] weights[j], 0 <= digits[j] < p_j."""
     if len(residues) != len(basis.primes):
         raise ValueError("got %d residues for %d primes" % (len(residues), len(basis.primes)))
-    vals = np.array([[int(x) % p] for x, p in zip(residues, basis.primes)], dtype=np.int64)
-    value = device_lift(native.to_device_u32(vals), basis.primes, 1, 1)[0]
+    vals = np.array([[int(x) % p] for x, p in zip(residues, basis.primes)], dtype=object)
+    value = device_lift(native.to_device_words(vals, wide_primes(basis.primes)), basis.primes, 1, 1)[0]
     if value < 0:
         value += basis.product
     digits = []
@@ -148,5 +157,5 @@ def combine_tensor(residue_tensors) -> CoeffTensor:
     basis = build_basis([t.prime.p for t in residue_tensors])
     n = residue_tensors[0].size
     stacked = np.stack([np.asarray(t.residues, dtype=object).astype(np.int64) for t in residue_tensors])
-    coeffs = device_lift(native.to_device_u32(stacked), basis.primes, n, n)
+    coeffs = device_lift(native.to_device_words(stacked, wide_primes(basis.primes)), basis.primes, n, n)
     return CoeffTensor(tuple(shape), tuple(coeffs), tuple(names))

@@ -186,16 +186,41 @@ int32_t pdb_device_sm_count(int32_t device) {
 
 int32_t pdb_prime_ctx_create(uint64_t p, uint64_t omega, int32_t q, pdb_prime_ctx** out) {
   if (!out) { set_error("null output pointer"); return -2; }
-  if (p < 2 || p >= (1ull << 31)) {
-    set_error("modulus %llu outside the 32-bit kernel range (p < 2^31)", (unsigned long long)p);
+  if (p < 2 || p >= (1ull << 62)) {
+    set_error("modulus %llu outside the kernel range (p < 2^62)", (unsigned long long)p);
     return -2;
   }
-  if (q < 0 || q > 30 || omega >= p) { set_error("invalid prime spec"); return -2; }
+  const bool wide = p >= (1ull << 31);
+  if (wide && !(p & 1)) { set_error("wide modulus %llu must be odd", (unsigned long long)p); return -2; }
+  if (q < 0 || q > (wide ? 62 : 30) || omega >= p) { set_error("invalid prime spec"); return -2; }
   auto* c = new pdb_prime_ctx();
   c->p = p;
   c->omega = omega;
   c->q = q;
-  c->m = make_mod32((uint32_t)p);
+  c->wide = wide;
+  if (wide) c->m64 = make_mod64(p);
+  else c->m = make_mod32((uint32_t)p);
+  cudaGetDevice(&c->device);
+  int sms = pdb_device_sm_count(c->device);
+  c->sms = sms > 0 ? sms : 148;
+  *out = c;
+  return 0;
+}
+
+int32_t pdb_prime_ctx_create_wide(uint64_t p, uint64_t omega, int32_t q, pdb_prime_ctx** out) {
+  // a u64-kernel context for any odd prime (mixed prime sets share one residue width)
+  if (!out) { set_error("null output pointer"); return -2; }
+  if (p < 3 || !(p & 1) || p >= (1ull << 62)) {
+    set_error("wide context needs an odd modulus 3 <= p < 2^62, got %llu", (unsigned long long)p);
+    return -2;
+  }
+  if (q < 0 || q > 62 || omega >= p) { set_error("invalid prime spec"); return -2; }
+  auto* c = new pdb_prime_ctx();
+  c->p = p;
+  c->omega = omega;
+  c->q = q;
+  c->wide = true;
+  c->m64 = make_mod64(p);
   cudaGetDevice(&c->device);
   int sms = pdb_device_sm_count(c->device);
   c->sms = sms > 0 ? sms : 148;
@@ -207,19 +232,30 @@ int32_t pdb_prime_ctx_destroy(pdb_prime_ctx* ctx) {
   if (!ctx) return 0;
   for (auto& T : ctx->tw)
     if (T.fwd) cudaFree(T.fwd);
+  for (auto& T : ctx->tw64)
+    if (T.fwd) cudaFree(T.fwd);
   delete ctx;
   return 0;
 }
 
 int32_t pdb_prime_ctx_prepare(pdb_prime_ctx* ctx, int64_t n) {
   if (!ctx) { set_error("null context"); return -2; }
+  if (ctx->wide) return ctx_twiddles64(ctx, (int)n) ? 0 : -2;
   return ctx_twiddles(ctx, (int)n) ? 0 : -2;
+}
+
+// the u32 entry points take contexts of primes < 2^31 only
+static bool narrow_ctx(const pdb_prime_ctx* ctx) {
+  if (!ctx) { set_error("null context"); return false; }
+  if (ctx->wide) { set_error("context holds a prime >= 2^31: use the _u64 entry points"); return false; }
+  return true;
 }
 
 int32_t pdb_ntt_multi_u32(pdb_prime_ctx* ctx, uint32_t* data, int64_t batch, int32_t ndim,
                           const int64_t* dims, const int64_t* extents, uint32_t axis_mask,
                           int32_t inverse, void* stream) {
-  if (!ctx || ndim < 0 || ndim > PDB_MAX_DIMS || batch < 0) { set_error("invalid NTT arguments"); return -2; }
+  if (!narrow_ctx(ctx)) return -2;
+  if (ndim < 0 || ndim > PDB_MAX_DIMS || batch < 0) { set_error("invalid NTT arguments"); return -2; }
   for (int a = 0; a < ndim; ++a)
     if ((axis_mask >> a) & 1)
       if (!ctx_twiddles(ctx, (int)dims[a])) return -2;
@@ -235,7 +271,8 @@ int32_t pdb_ntt_multi_u32(pdb_prime_ctx* ctx, uint32_t* data, int64_t batch, int
 int32_t pdb_reduce_scatter_u32(pdb_prime_ctx* ctx, const uint32_t* mag, const uint8_t* neg,
                                const int64_t* pos, int64_t count, int32_t limbs, uint32_t* dst,
                                void* stream) {
-  if (!ctx || limbs < 1) { set_error("invalid reduce arguments"); return -2; }
+  if (!narrow_ctx(ctx)) return -2;
+  if (limbs < 1) { set_error("invalid reduce arguments"); return -2; }
   return reduce_scatter(ctx, mag, neg, pos, count, limbs, dst, (cudaStream_t)stream);
 }
 
@@ -244,7 +281,7 @@ size_t pdb_det_scratch_bytes(int32_t r, int64_t nodes) { return det_scratch_byte
 int32_t pdb_det_batch_u32(pdb_prime_ctx* ctx, const uint32_t* grids, int64_t grid_stride,
                           const int32_t* entry_ids, int32_t r, int64_t node_lo, int64_t nodes,
                           uint32_t* out, void* scratch, size_t scratch_bytes, void* stream) {
-  if (!ctx) { set_error("null context"); return -2; }
+  if (!narrow_ctx(ctx)) return -2;
   StagedSrc src{grids, grid_stride};
   return det_run(ctx, src, entry_ids, r, node_lo, nodes, out, scratch, scratch_bytes, (cudaStream_t)stream);
 }
@@ -253,7 +290,8 @@ int32_t pdb_eval_det_fused_u32(pdb_prime_ctx* ctx, const uint32_t* partial, int6
                                int32_t ncoef, int32_t entries, int32_t n_last, const int32_t* entry_ids, int32_t r,
                                int64_t node_lo, int64_t nodes, uint32_t* out, void* scratch,
                                size_t scratch_bytes, void* stream) {
-  if (!ctx || ncoef < 1 || entries < 1) { set_error("invalid fused arguments"); return -2; }
+  if (!narrow_ctx(ctx)) return -2;
+  if (ncoef < 1 || entries < 1) { set_error("invalid fused arguments"); return -2; }
   const Twiddles* T = ctx_twiddles(ctx, n_last);
   if (!T) return -2;
   FusedSrc src{partial, outer, ncoef, entries, n_last, T->full, T->full_s, ctx->m.p};
@@ -263,7 +301,7 @@ int32_t pdb_eval_det_fused_u32(pdb_prime_ctx* ctx, const uint32_t* partial, int6
 int32_t pdb_condense_u32(pdb_prime_ctx* ctx, const uint32_t* mat, int32_t r, uint32_t* trail_vals,
                          int32_t* trail_cols, uint32_t* det_out, void* scratch, size_t scratch_bytes,
                          void* stream) {
-  if (!ctx) { set_error("null context"); return -2; }
+  if (!narrow_ctx(ctx)) return -2;
   return condense_run(ctx, mat, r, trail_vals, trail_cols, det_out, scratch, scratch_bytes,
                       (cudaStream_t)stream);
 }

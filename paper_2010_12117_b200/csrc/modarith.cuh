@@ -161,3 +161,56 @@ inline Mod32 make_mod32(uint32_t p) {
   m.m64 = (uint64_t)(((unsigned __int128)1 << 64) / p);
   return m;
 }
+
+// ---- 64-bit moduli (the wide path: 2^31 <= p < 2^62) ---------------------------
+// Montgomery arithmetic with R = 2^64 in the subtractive form:
+//   mont64(a, b) = a*b*2^-64 mod p,  canonical for a, b < p < 2^62
+// (hi(a*b) < p/4, so hi + p - hi(q*p) < 1.25 p: one conditional subtraction).
+struct Mod64 {
+  uint64_t p;
+  uint64_t qinv;   // p^-1 mod 2^64
+  uint64_t r1;     // 2^64 mod p   (Montgomery one)
+  uint64_t r2;     // 2^128 mod p  (to Montgomery form)
+  uint64_t r96;    // 2^96 mod p   (Montgomery form of 2^32: limb Horner)
+};
+
+PDB_HD uint64_t mont64(uint64_t a, uint64_t b, const Mod64& m) {
+  const uint64_t lo = a * b;
+  const uint64_t hi = umulhi64(a, b);
+  const uint64_t q = lo * m.qinv;
+  const uint64_t v = hi + m.p - umulhi64(q, m.p);
+  return v >= m.p ? v - m.p : v;
+}
+
+PDB_HD uint64_t add_mod64(uint64_t a, uint64_t b, uint64_t p) {
+  const uint64_t s = a + b;
+  return s >= p ? s - p : s;
+}
+
+PDB_HD uint64_t sub_mod64(uint64_t a, uint64_t b, uint64_t p) { return a >= b ? a - b : a + p - b; }
+
+PDB_HD uint64_t to_mont64(uint64_t x, const Mod64& m) { return mont64(x, m.r2, m); }
+PDB_HD uint64_t from_mont64(uint64_t x, const Mod64& m) { return mont64(x, 1, m); }
+
+// (a R)^e R^-1 ... i.e. Montgomery power: aR -> a^e R
+PDB_HD uint64_t mont_pow64(uint64_t aR, uint64_t e, const Mod64& m) {
+  uint64_t r = m.r1, b = aR;
+  while (e) {
+    if (e & 1) r = mont64(r, b, m);
+    b = mont64(b, b, m);
+    e >>= 1;
+  }
+  return r;
+}
+
+inline Mod64 make_mod64(uint64_t p) {
+  Mod64 m;
+  m.p = p;
+  uint64_t inv = 1;   // Newton iteration for p^-1 mod 2^64 (p odd)
+  for (int i = 0; i < 6; ++i) inv *= 2u - p * inv;
+  m.qinv = inv;
+  m.r1 = (uint64_t)(((unsigned __int128)1 << 64) % p);
+  m.r2 = (uint64_t)((unsigned __int128)m.r1 * m.r1 % p);
+  m.r96 = (uint64_t)((unsigned __int128)m.r2 * ((uint64_t)1 << 32) % p);
+  return m;
+}

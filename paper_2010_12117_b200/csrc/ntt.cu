@@ -20,31 +20,6 @@
 
 namespace pdb {
 
-struct AxisGeom {
-  int64_t inner;           // product of dims after the axis
-  int32_t nbox;            // number of box dims describing active outer lines
-  int64_t box_ext[PDB_MAX_DIMS + 1];   // active extent per outer dim (slowest first)
-  int64_t box_dim[PDB_MAX_DIMS + 1];   // full dim per outer dim
-  int64_t active_outer;    // product of box_ext
-};
-
-__device__ __forceinline__ int64_t outer_offset(int64_t c, const AxisGeom& g) {
-  // compact active index -> real outer line index (mixed radix)
-  int64_t off = 0, mul = 1;
-  for (int d = g.nbox - 1; d >= 0; --d) {
-    int64_t e = g.box_ext[d];
-    int64_t i = c % e;
-    c /= e;
-    off += i * mul;
-    mul *= g.box_dim[d];
-  }
-  return off;
-}
-
-__device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) {
-  return bits ? (__brev(x) >> (32 - bits)) : 0u;
-}
-
 template <bool INV>
 __global__ void __launch_bounds__(256)
 ntt_axis_smem(uint32_t* __restrict__ data, AxisGeom g, int N, int logN, int TI, int LO,

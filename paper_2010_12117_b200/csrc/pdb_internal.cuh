@@ -26,10 +26,21 @@ struct Twiddles {
   uint32_t ninv = 1, ninv_s = 0;  // N^-1 and its companion
 };
 
+// Per-length tables of a wide prime (p >= 2^31): Montgomery forms (R = 2^64).
+struct Twiddles64 {
+  int N = 0;
+  uint64_t* fwd = nullptr;   // w^j R, j < N/2
+  uint64_t* inv = nullptr;   // w^-j R
+  uint64_t ninv = 0;         // N^-1 R
+};
+
 struct PrimeCtx {
   uint64_t p = 0, omega = 0;
   int q = 0;
+  bool wide = false;         // p >= 2^31: the u64 kernels (wide.cu)
   Mod32 m;
+  Mod64 m64;
+  Twiddles64 tw64[64];
   int device = 0;
   int sms = 148;
   Twiddles tw[32];
@@ -37,6 +48,34 @@ struct PrimeCtx {
 };
 
 const Twiddles* ctx_twiddles(PrimeCtx* ctx, int N);
+const Twiddles64* ctx_twiddles64(PrimeCtx* ctx, int N);
+
+// ---- one axis of a batched row-major tensor (shared by the u32 and u64 NTTs) ----
+struct AxisGeom {
+  int64_t inner;           // product of dims after the axis
+  int32_t nbox;            // number of box dims describing active outer lines
+  int64_t box_ext[PDB_MAX_DIMS + 1];   // active extent per outer dim (slowest first)
+  int64_t box_dim[PDB_MAX_DIMS + 1];   // full dim per outer dim
+  int64_t active_outer;    // product of box_ext
+};
+
+__device__ __forceinline__ int64_t outer_offset(int64_t c, const AxisGeom& g) {
+  // compact active index -> real outer line index (mixed radix)
+  int64_t off = 0, mul = 1;
+  for (int d = g.nbox - 1; d >= 0; --d) {
+    int64_t e = g.box_ext[d];
+    int64_t i = c % e;
+    c /= e;
+    off += i * mul;
+    mul *= g.box_dim[d];
+  }
+  return off;
+}
+
+__device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) {
+  return bits ? (__brev(x) >> (32 - bits)) : 0u;
+}
+
 
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);

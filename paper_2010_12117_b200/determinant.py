@@ -1,5 +1,6 @@
 """Determinants mod p -- drop-in for the reference's `determinant.py`
-(reference lines 23-169), computed by `pdb_det_batch_u32` / `pdb_condense_u32`.
+(reference lines 23-169), computed by `pdb_det_batch_u32` / `pdb_condense_u32` (and their
+`_u64` twins for primes >= 2^31).
 
 `det_grid` keeps the reference's signature and errors; `chunk_size` and
 `workers` are accepted and ignored (the result never depended on them in the
@@ -57,13 +58,16 @@ def condense(m: ModMatrix):
     torch = native._torch()
     ctx = native.prime_context(m.prime)
     r = m.r
-    mat = native.to_device_u32(np.array(m.entries, dtype=np.int64).reshape(-1))
-    vals = torch.zeros(r, dtype=torch.int32, device=mat.device)
+    wide = ctx.wide
+    word = native.word_dtype(wide)
+    mat = native.to_device_words(np.array([int(v) for row in m.entries for v in row], dtype=object), wide)
+    vals = torch.zeros(r, dtype=word, device=mat.device)
     cols = torch.zeros(r, dtype=torch.int32, device=mat.device)
-    det = torch.zeros(1, dtype=torch.int32, device=mat.device)
-    scratch = native.scratch_tensor(4 * r * r + 256 + 512 * r * r + 256)
+    det = torch.zeros(1, dtype=word, device=mat.device)
+    nbytes = 4 * r * r + 256 + (native.det_scratch_bytes(r, 1, True) if wide else 512 * r * r + 256)
+    scratch = native.scratch_tensor(nbytes)
     native.condense(ctx, mat, r, vals, cols, det, scratch)
-    vals_h = native.to_host_u32(vals).tolist()
+    vals_h = native.to_host_words(vals, wide).tolist()
     cols_h = cols.cpu().numpy().tolist()
     records, used = [], []
     for i in range(r):
@@ -73,7 +77,7 @@ def condense(m: ModMatrix):
         flips = sum(1 for u in used if u > c) % 2 == 1
         records.append(PivotRecord(i, int(vals_h[i]), c, flips))
         used.append(c)
-    return int(native.to_host_u32(det)[0]), records
+    return int(native.to_host_words(det, wide)[0]), records
 
 
 def det_mod(m: ModMatrix) -> int:
@@ -101,9 +105,14 @@ def det_grid(entry_grids, r: int, prime: PrimeSpec, *, entry_ids=None, chunk_siz
         return np.empty(0, dtype=dtype)
     torch = native._torch()
     ctx = native.prime_context(prime)
-    dev = native.to_device_u32(np.stack(grids).astype(np.int64) % prime.p)
+    wide = ctx.wide
+    p = prime.p
+    stacked = np.stack(grids)
+    stacked = np.array([int(v) % p for v in stacked.reshape(-1)], dtype=object).reshape(stacked.shape) \
+        if stacked.dtype == object else stacked.astype(np.int64) % p
+    dev = native.to_device_words(stacked, wide)
     ids = torch.tensor(entry_ids, dtype=torch.int32, device=dev.device)
-    out = torch.empty(nodes, dtype=torch.int32, device=dev.device)
-    scratch = native.scratch_tensor(native.det_scratch_bytes(r, nodes))
+    out = torch.empty(nodes, dtype=native.word_dtype(wide), device=dev.device)
+    scratch = native.scratch_tensor(native.det_scratch_bytes(r, nodes, wide))
     native.det_batch(ctx, dev, nodes, ids, r, 0, nodes, out, scratch)
-    return native.to_host_u32(out).astype(dtype)
+    return native.to_host_words(out, wide).astype(dtype)

@@ -35,7 +35,7 @@ import numpy as np
 
 from . import native, shard
 from .checkpoint import Workspace, digest_of
-from .crt import device_lift
+from .crt import device_lift, wide_primes
 from .errors import StaleWorkspaceError
 from .layout import CoeffTensor, PolyMatrix, residue_dtype
 from .planner import Plan, PipelineConfig, StageTimings, plan
@@ -125,7 +125,11 @@ class DevicePlan:
         self.vn = len(self.shape)
         self.nodes = pl.node_count
         self.k = m.k
-        self.staged = staged or self.vn == 0
+        # primes >= 2^31 (reference int64/object dtype paths): u64 residues and kernels,
+        # staged layout (the fused det kernel is the u32 throughput path)
+        self.wide = wide_primes([s.p for s in pl.primes])
+        self.word = native.word_dtype(self.wide)
+        self.staged = staged or self.vn == 0 or self.wide
         entries, coeffs = [], []
         for e, t in enumerate(m.unique_entries):
             for exps, c in t.terms().items():
@@ -212,19 +216,19 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
     nodes = dp.nodes
     P = pl.prime_count
     mine = shard.my_primes(P, rank, size)
-    residues = torch.empty((len(mine), nodes), dtype=torch.int32, device=device)
-    work = torch.empty(dp.buffer_words() or 1, dtype=torch.int32, device=device)
+    residues = torch.empty((len(mine), nodes), dtype=dp.word, device=device)
+    work = torch.empty(dp.buffer_words() or 1, dtype=dp.word, device=device)
     det_chunk = nodes if dp.staged else min(nodes, FUSED_CHUNK)
-    det_buf = torch.empty(nodes, dtype=torch.int32, device=device)
-    scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, det_chunk), device)
+    det_buf = torch.empty(nodes, dtype=dp.word, device=device)
+    scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, det_chunk, dp.wide), device)
     events = []
     for row, pi in enumerate(mine):
         spec = pl.primes[pi]
         unit = "p%d/ifft" % pi
         if ws is not None and ws.has(unit):
-            residues[row].copy_(native.to_device_u32(_load_grid(ws, unit, pl)))
+            residues[row].copy_(native.to_device_words(_load_grid(ws, unit, pl), dp.wide))
             continue
-        ctx = native.prime_context(spec, device.index)
+        ctx = native.prime_context(spec, device.index, dp.wide)
         t0 = _Timer(torch, stream).mark()
         _fft_stage(dp, ctx, work, ws, pi, cfg)
         t1 = _Timer(torch, stream).mark()
@@ -235,7 +239,7 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
         t3 = _Timer(torch, stream).mark()
         events.append((t0, t1, t2, t3))
         if ws is not None:
-            ws.store_residues(unit, native.to_host_u32(residues[row]), pl.shape)
+            ws.store_residues(unit, native.to_host_words(residues[row], dp.wide), pl.shape)
         cfg._notify(unit)
     if size > 1:
         residues = shard.gather_residues(residues, P, rank, size)
@@ -270,7 +274,7 @@ def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
         unit = "p%d/fft/e%d" % (pi, eid)
         if ws is not None and ws.has(unit):
             grid = _load_grid(ws, unit, pl)
-            work[eid * dp.nodes:(eid + 1) * dp.nodes].copy_(native.to_device_u32(grid))
+            work[eid * dp.nodes:(eid + 1) * dp.nodes].copy_(native.to_device_words(grid, dp.wide))
         else:
             todo.append(eid)
     if not todo:
@@ -290,7 +294,8 @@ def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
     for eid in todo:
         unit = "p%d/fft/e%d" % (pi, eid)
         if ws is not None:
-            ws.store_residues(unit, native.to_host_u32(work[eid * dp.nodes:(eid + 1) * dp.nodes]), pl.shape)
+            ws.store_residues(unit, native.to_host_words(work[eid * dp.nodes:(eid + 1) * dp.nodes], dp.wide),
+                              pl.shape)
         cfg._notify(unit)
 
 
@@ -298,7 +303,7 @@ def _det_stage(dp: DevicePlan, ctx, work, det_buf, scratch, chunk, ws, pi, cfg):
     pl = dp.pl
     unit = "p%d/det" % pi
     if ws is not None and ws.has(unit):
-        det_buf.copy_(native.to_device_u32(_load_grid(ws, unit, pl)))
+        det_buf.copy_(native.to_device_words(_load_grid(ws, unit, pl), dp.wide))
         return
     if dp.staged:
         native.det_batch(ctx, work, dp.nodes, dp.ids, pl.r, 0, dp.nodes, det_buf, scratch)
@@ -310,7 +315,7 @@ def _det_stage(dp: DevicePlan, ctx, work, det_buf, scratch, chunk, ws, pi, cfg):
                                   det_buf[lo:lo + cnt], scratch)
     if dp.staged:   # fused mode has no det (or fft) units: it checkpoints per prime
         if ws is not None:
-            ws.store_residues(unit, native.to_host_u32(det_buf), pl.shape)
+            ws.store_residues(unit, native.to_host_words(det_buf, dp.wide), pl.shape)
         cfg._notify(unit)
 
 
@@ -348,14 +353,14 @@ class PrimeStages:
         self.m, self.pl = m, pl
         self.dp = DevicePlan(m, pl, self.device, staged)
         dp = self.dp
-        self.work = torch.empty(dp.buffer_words() or 1, dtype=torch.int32, device=self.device)
+        self.work = torch.empty(dp.buffer_words() or 1, dtype=dp.word, device=self.device)
         self.chunk = dp.nodes if dp.staged else min(dp.nodes, FUSED_CHUNK)
-        self.det = torch.empty(dp.nodes, dtype=torch.int32, device=self.device)
-        self.scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, self.chunk), self.device)
+        self.det = torch.empty(dp.nodes, dtype=dp.word, device=self.device)
+        self.scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, self.chunk, dp.wide), self.device)
         self._cfg = PipelineConfig()
 
     def ctx(self, pi):
-        return native.prime_context(self.pl.primes[pi], self.device.index)
+        return native.prime_context(self.pl.primes[pi], self.device.index, self.dp.wide)
 
     def forward(self, pi):
         _fft_stage(self.dp, self.ctx(pi), self.work, None, pi, self._cfg)

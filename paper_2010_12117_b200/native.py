@@ -19,7 +19,12 @@ from .errors import DeviceError
 
 LIB_NAME = "libpolydet_b200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
-U32_LIMIT = 2**31  # device kernels: p < 2^31
+U32_LIMIT = 2**31   # u32 kernels: p < 2^31
+WIDE_LIMIT = 2**62  # u64 kernels (the wide path): p < 2^62
+
+
+def needs_wide(p: int) -> bool:
+    return p >= U32_LIMIT
 
 _lib = None
 _lock = threading.Lock()
@@ -48,6 +53,18 @@ _SIGNATURES = {
     "pdb_crt_mrc_u32": (_c_i32, [_c_vp, _c_i32, _c_i64, _c_i64, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp,
                                  _c_size, _c_vp]),
     "pdb_mulmod_peak": (_c_i32, [_c_u32, _c_i32, ctypes.POINTER(ctypes.c_double), _c_vp]),
+    # the wide path (2^31 <= p < 2^62): u64 twins
+    "pdb_prime_ctx_create_wide": (_c_i32, [_c_u64, _c_u64, _c_i32, ctypes.POINTER(_c_vp)]),
+    "pdb_ntt_multi_u64": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp, _c_u32, _c_i32, _c_vp]),
+    "pdb_reduce_scatter_u64": (_c_i32, [_c_vp, _c_vp, _c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp]),
+    "pdb_det_scratch_bytes_u64": (_c_size, [_c_i32, _c_i64]),
+    "pdb_det_batch_u64": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i32, _c_i64, _c_i64, _c_vp,
+                                   _c_vp, _c_size, _c_vp]),
+    "pdb_condense_u64": (_c_i32, [_c_vp, _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_vp, _c_size, _c_vp]),
+    "pdb_crt_limbs_u64": (_c_i32, [_c_i32]),
+    "pdb_crt_scratch_bytes_u64": (_c_size, [_c_i32]),
+    "pdb_crt_mrc_u64": (_c_i32, [_c_vp, _c_i32, _c_i64, _c_i64, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp,
+                                 _c_size, _c_vp]),
 }
 
 
@@ -126,15 +143,18 @@ def host_i64(values) -> ctypes.Array:
 class PrimeContext:
     """Device twiddle tables + constants of one prime (reference TwiddleTable)."""
 
-    def __init__(self, p: int, omega: int, q: int, device: int):
-        if p >= U32_LIMIT:
-            raise ValueError("modulus %d exceeds the 32-bit device kernels (p < 2^31)" % p)
+    def __init__(self, p: int, omega: int, q: int, device: int, wide: bool = None):
+        if p >= WIDE_LIMIT:
+            raise ValueError("modulus %d exceeds the device kernels (p < 2^62)" % p)
+        wide = needs_wide(p) if wide is None else bool(wide)
         lib = load_library()
         torch = _torch()
         handle = ctypes.c_void_p()
+        create = lib.pdb_prime_ctx_create_wide if wide else lib.pdb_prime_ctx_create
         with torch.cuda.device(device):
-            check(lib.pdb_prime_ctx_create(p, omega, q, ctypes.byref(handle)), "prime context")
+            check(create(p, omega, q, ctypes.byref(handle)), "prime context")
         self.handle = handle
+        self.wide = wide
         self.p, self.omega, self.q, self.device = p, omega, q, device
         self._lib = lib
 
@@ -154,14 +174,17 @@ class PrimeContext:
 _contexts: dict = {}
 
 
-def prime_context(spec, device=None) -> PrimeContext:
+def prime_context(spec, device=None, wide=None) -> PrimeContext:
+    """Cached context of one prime; wide=True forces the u64 kernels (a prime
+    set mixing p < 2^31 and p >= 2^31 shares one residue width)."""
     torch = _torch()
     dev = torch.cuda.current_device() if device is None else int(device)
-    key = (spec.p, spec.omega, spec.q, dev)
+    wide = needs_wide(spec.p) if wide is None else bool(wide) or needs_wide(spec.p)
+    key = (spec.p, spec.omega, spec.q, dev, wide)
     with _lock:
         ctx = _contexts.get(key)
     if ctx is None:
-        ctx = PrimeContext(spec.p, spec.omega, spec.q, dev)
+        ctx = PrimeContext(spec.p, spec.omega, spec.q, dev, wide)
         with _lock:
             _contexts[key] = ctx
     return ctx
@@ -176,26 +199,30 @@ def ntt_multi(ctx: PrimeContext, data, batch: int, dims, extents, axes, inverse:
     for a in axes:
         mask |= 1 << a
     ext = host_i64(extents) if extents is not None else None
-    check(lib.pdb_ntt_multi_u32(ctx.handle, ptr(data), int(batch), nd, host_i64(dims),
-                                ext, mask, int(bool(inverse)), stream_handle(stream)), "ntt")
+    fn = lib.pdb_ntt_multi_u64 if ctx.wide else lib.pdb_ntt_multi_u32
+    check(fn(ctx.handle, ptr(data), int(batch), nd, host_i64(dims), ext, mask, int(bool(inverse)),
+             stream_handle(stream)), "ntt")
 
 
 def reduce_scatter(ctx: PrimeContext, mag, neg, pos, count: int, limbs: int, dst, stream=None):
     lib = load_library()
-    check(lib.pdb_reduce_scatter_u32(ctx.handle, ptr(mag), ptr(neg), ptr(pos), int(count), int(limbs),
-                                     ptr(dst), stream_handle(stream)), "reduce_scatter")
+    fn = lib.pdb_reduce_scatter_u64 if ctx.wide else lib.pdb_reduce_scatter_u32
+    check(fn(ctx.handle, ptr(mag), ptr(neg), ptr(pos), int(count), int(limbs), ptr(dst), stream_handle(stream)),
+          "reduce_scatter")
 
 
-def det_scratch_bytes(r: int, nodes: int) -> int:
-    return int(load_library().pdb_det_scratch_bytes(int(r), int(nodes)))
+def det_scratch_bytes(r: int, nodes: int, wide: bool = False) -> int:
+    lib = load_library()
+    fn = lib.pdb_det_scratch_bytes_u64 if wide else lib.pdb_det_scratch_bytes
+    return int(fn(int(r), int(nodes)))
 
 
 def det_batch(ctx: PrimeContext, grids, grid_stride: int, ids, r: int, node_lo: int, nodes: int,
               out, scratch, stream=None):
     lib = load_library()
-    check(lib.pdb_det_batch_u32(ctx.handle, ptr(grids), int(grid_stride), ptr(ids), int(r), int(node_lo),
-                                int(nodes), ptr(out), ptr(scratch), scratch.numel() * scratch.element_size(),
-                                stream_handle(stream)), "det")
+    fn = lib.pdb_det_batch_u64 if ctx.wide else lib.pdb_det_batch_u32
+    check(fn(ctx.handle, ptr(grids), int(grid_stride), ptr(ids), int(r), int(node_lo), int(nodes), ptr(out),
+             ptr(scratch), scratch.numel() * scratch.element_size(), stream_handle(stream)), "det")
 
 
 def eval_det_fused(ctx: PrimeContext, partial, outer: int, ncoef: int, entries: int, n_last: int, ids, r: int,
@@ -210,25 +237,32 @@ def eval_det_fused(ctx: PrimeContext, partial, outer: int, ncoef: int, entries: 
 
 def condense(ctx: PrimeContext, mat, r: int, trail_vals, trail_cols, det_out, scratch, stream=None):
     lib = load_library()
-    check(lib.pdb_condense_u32(ctx.handle, ptr(mat), int(r), ptr(trail_vals), ptr(trail_cols),
-                               ptr(det_out), ptr(scratch), scratch.numel() * scratch.element_size(),
-                               stream_handle(stream)), "condense")
+    fn = lib.pdb_condense_u64 if ctx.wide else lib.pdb_condense_u32
+    check(fn(ctx.handle, ptr(mat), int(r), ptr(trail_vals), ptr(trail_cols), ptr(det_out), ptr(scratch),
+             scratch.numel() * scratch.element_size(), stream_handle(stream)), "condense")
 
 
-def crt_limbs(nprimes: int) -> int:
-    return int(load_library().pdb_crt_limbs(int(nprimes)))
-
-
-def crt_scratch_bytes(nprimes: int) -> int:
-    return int(load_library().pdb_crt_scratch_bytes(int(nprimes)))
-
-
-def crt_mrc(residues, nprimes: int, n: int, stride: int, primes, limbs, L: int, neg, scratch, stream=None):
+def crt_limbs(nprimes: int, wide: bool = False) -> int:
     lib = load_library()
-    hp = (ctypes.c_uint32 * nprimes)(*[int(p) for p in primes])
-    check(lib.pdb_crt_mrc_u32(ptr(residues), int(nprimes), int(n), int(stride), hp, ptr(limbs), int(L),
-                              ptr(neg), ptr(scratch), scratch.numel() * scratch.element_size(),
-                              stream_handle(stream)), "crt")
+    return int((lib.pdb_crt_limbs_u64 if wide else lib.pdb_crt_limbs)(int(nprimes)))
+
+
+def crt_scratch_bytes(nprimes: int, wide: bool = False) -> int:
+    lib = load_library()
+    return int((lib.pdb_crt_scratch_bytes_u64 if wide else lib.pdb_crt_scratch_bytes)(int(nprimes)))
+
+
+def crt_mrc(residues, nprimes: int, n: int, stride: int, primes, limbs, L: int, neg, scratch, stream=None,
+            wide: bool = False):
+    lib = load_library()
+    if wide:
+        hp = (ctypes.c_uint64 * nprimes)(*[int(p) for p in primes])
+        fn = lib.pdb_crt_mrc_u64
+    else:
+        hp = (ctypes.c_uint32 * nprimes)(*[int(p) for p in primes])
+        fn = lib.pdb_crt_mrc_u32
+    check(fn(ptr(residues), int(nprimes), int(n), int(stride), hp, ptr(limbs), int(L), ptr(neg), ptr(scratch),
+             scratch.numel() * scratch.element_size(), stream_handle(stream)), "crt")
 
 
 def launch_count() -> int:
@@ -255,6 +289,30 @@ def to_device_u32(values, device=None):
 
 def to_host_u32(t) -> np.ndarray:
     return t.detach().cpu().numpy().view(np.uint32)
+
+
+def word_dtype(wide: bool):
+    """Device residue word: int32 (u32 kernels) or int64 (u64 kernels, values < 2^62)."""
+    torch = _torch()
+    return torch.int64 if wide else torch.int32
+
+
+def to_device_words(values, wide: bool, device=None):
+    """Residues (numpy, any int or object dtype) -> device tensor of the path's word."""
+    if not wide:
+        return to_device_u32(values, device)
+    torch = _torch()
+    arr = np.asarray(values)
+    arr = np.array([int(v) for v in arr.reshape(-1)], dtype=np.int64).reshape(arr.shape) if arr.dtype == object \
+        else np.array(arr, dtype=np.int64)
+    return torch.from_numpy(arr).to(device or torch.cuda.current_device())
+
+
+def to_host_words(t, wide: bool) -> np.ndarray:
+    """Device residues -> numpy uint32 / uint64."""
+    if not wide:
+        return to_host_u32(t)
+    return t.detach().cpu().numpy().view(np.uint64)
 
 
 def scratch_tensor(nbytes: int, device=None):

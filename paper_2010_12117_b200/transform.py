@@ -66,9 +66,9 @@ def _device_transform(values: np.ndarray, shape: tuple, table: TwiddleTable, inv
     if not shape:
         return np.array(values, copy=True)
     ctx = table.device()
-    data = native.to_device_u32(values)
+    data = native.to_device_words(values, ctx.wide)
     native.ntt_multi(ctx, data, 1, shape, None, range(len(shape)), inverse)
-    return native.to_host_u32(data).astype(residue_dtype(table.prime))
+    return native.to_host_words(data, ctx.wide).astype(residue_dtype(table.prime))
 
 
 def _as_row(data, table: TwiddleTable) -> np.ndarray:

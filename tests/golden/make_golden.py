@@ -234,6 +234,71 @@ def workspace_case():
     _write("workspace.json", {"input": m.to_dict(), "units": units, "manifest": manifest, "files": files})
 
 
+def wide_cases():
+    """Primes >= 2^31: the reference's int64 (p <= 3.04e9) and object-dtype
+    (p up to 2^62) paths -- NTTs, determinants, a mixed-prime CRT, end-to-end
+    runs at prime_start = 2^61 and a checkpointed workspace's file hashes
+    (reference tests: test_transform.py:221-230, test_determinant.py:105-114,
+    test_crt.py:147-153, test_pipeline.py:149-153, test_workspace.py:179-189)."""
+    rng = random.Random(15)
+    out = {"ntt": [], "det": [], "crt": [], "runs": []}
+    specs = [ref.find_fourier_primes(4, 1, start=2**61, min_count=1)[0],       # object dtype
+             ref.find_fourier_primes(10, 1, start=2**31 + 1, min_count=1)[0],  # int64, > 2^31
+             ref.find_fourier_primes(6, 1, start=3 * 10**9, min_count=1)[0]]    # object, < 2^32
+    for spec in specs:
+        table = ref.TwiddleTable(spec)
+        dt = ref.tensor.residue_dtype(spec)
+        for shape in [(16,), (4, 4), (2, 8, 1), (1,), ()]:
+            size = int(np.prod(shape)) if shape else 1
+            vals = [rng.randrange(spec.p) for _ in range(size)]
+            mt = ref.ModTensor(shape, np.array(vals, dtype=dt), spec, tuple("v%d" % i for i in range(len(shape))))
+            out["ntt"].append({"prime": [spec.p, spec.c, spec.q, spec.omega], "shape": list(shape), "input": vals,
+                               "forward": [int(v) for v in ref.ntt_forward_multi(mt, table).residues.tolist()],
+                               "inverse": [int(v) for v in ref.ntt_inverse_multi(mt, table).residues.tolist()],
+                               "dtype": str(dt)})
+        for r in (1, 2, 3, 4, 6, 9, 12):
+            nodes = 12
+            mats = [[[rng.randrange(spec.p) for _ in range(r)] for _ in range(r)] for _ in range(nodes)]
+            if r >= 2:
+                mats[1][r - 1] = list(mats[1][0])
+                mats[2][0] = [0] * r
+                mats[3][0][0] = 0
+            grids = [[mats[n][e // r][e % r] for n in range(nodes)] for e in range(r * r)]
+            g = [np.array(x, dtype=dt) for x in grids]
+            det = ref.det_grid(g, r, spec)
+            out["det"].append({"prime": [spec.p, spec.c, spec.q, spec.omega], "r": r, "grids": grids,
+                               "expected": [int(v) for v in det], "dtype": str(det.dtype)})
+    for start in (2**61, 2**31 + 1):
+        cs = ref.find_fourier_primes(6, 1, start, min_count=3) + ref.find_fourier_primes(6, 1, 10**9, min_count=2)
+        product = 1
+        for sp in cs:
+            product *= sp.p
+        half = product // 2
+        vals = [rng.randint(-half + 1, half) for _ in range(30)] + [0, 1, -1, half, -half + 1]
+        tensors = [ref.reduce_mod(ref.CoeffTensor((len(vals),), tuple(vals), ("x",)), sp) for sp in cs]
+        res = ref.combine_tensor(tensors)
+        assert list(res.coeffs) == vals
+        out["crt"].append({"primes": [sp.p for sp in cs], "residues": [[int(v) for v in t.residues] for t in tensors],
+                           "expected": [str(v) for v in res.coeffs]})
+    for n in range(6):
+        r = rng.randint(1, 4)
+        vn = rng.randint(1, 2)
+        rows = random_matrix_terms(rng, r, vn, rng.randint(0, 3), 50, 3)
+        m = ref.poly_matrix(rows, tuple("xy"[:vn]))
+        result, _, pl = ref.run_report(m, ref.PipelineConfig(prime_start=2**61))
+        out["runs"].append({"name": "wide_%d" % n, "input": m.to_dict(), "config": {"prime_start": 2**61},
+                            "digest": pl.digest(), "shape": list(result.shape),
+                            "terms": _terms_json(result.terms())})
+    rows = random_matrix_terms(random.Random(13), 3, 2, 2, 25, 3)
+    m = ref.poly_matrix(rows, ("x", "y"))
+    with tempfile.TemporaryDirectory() as tmp:
+        units = []
+        ref.run(m, ref.PipelineConfig(prime_start=2**61, progress=units.append), workspace=Path(tmp) / "ws")
+        files = {q.name: hashlib.sha256(q.read_bytes()).hexdigest() for q in sorted((Path(tmp) / "ws").iterdir())}
+    out["workspace"] = {"input": m.to_dict(), "units": units, "files": files}
+    _write("wide.json", out)
+
+
 def c5_det_samples(n_nodes=24):
     """DET values of C5 at sampled nodes for primes 0 and 22 (direct evaluation).
 
@@ -295,6 +360,7 @@ def c3_full():
 if __name__ == "__main__":
     plans()
     primes()
+    wide_cases()
     ntt_cases()
     det_cases()
     crt_cases()
