@@ -352,3 +352,23 @@ def test_schwartz_zippel_full_size_c3(cuda):
             f = mat[i][c] * inv % q
             mat[i] = [(x - f * y) % q for x, y in zip(mat[i], mat[c])]
     assert lhs == det % q
+
+
+def test_predict_on_real_matrix(cuda):
+    """Reference test_pipeline.py:212-229: the forecast's fields and formula."""
+    from decimal import Decimal
+    from fractions import Fraction
+    from paper_2010_12117_b200 import predict, predicted_total
+    rng = random.Random(8)
+    rows = [[{(e,): rng.randint(-9, 9) for e in range(4)} for _ in range(2)] for _ in range(2)]
+    m = poly_matrix(rows, ("x",))
+    pl = plan(m)
+    forecast = predict(m, pl, sample_size=2)
+    assert forecast.prime_count == pl.prime_count and forecast.order == 2
+    assert len(forecast.sample_seconds) == 2
+    assert forecast.replication == Fraction(m.k, 4)
+    mean = sum(forecast.sample_seconds) / 2
+    assert forecast.total_seconds == predicted_total(pl.prime_count, pl.r, pl.unique_count, mean)
+    assert forecast.mean_rounded == Decimal(repr(mean)).quantize(Decimal("0.01"))
+    with pytest.raises(ValueError):
+        predict(m, pl, 0)

@@ -212,3 +212,13 @@ def test_native_ints_from_limbs_matches_python_path():
         h.ints_from_limbs(b"\0" * 8, np.zeros(1, np.int64).tobytes(), b"\0", 4, 1)
     with pytest.raises(IndexError):
         h.ints_from_limbs(b"\1\0\0\0", np.array([9], np.int64).tobytes(), b"\0", 4, 1)
+
+
+def test_predicted_total_reference_arithmetic():
+    """Reference test_pipeline.py:205-209 and acceptance criterion 2 (2088.96)."""
+    from paper_2010_12117_b200 import predicted_total
+    assert predicted_total(6, 16, 256, 1.36) == 2088.96
+    assert predicted_total(3, 4, 1, 0.5) == 1.5
+    assert predicted_total(2, 2, 4, 1.005) == pytest.approx(2 * 4 * 1.01)
+    with pytest.raises(ValueError):
+        predicted_total(1, 2, 5, 1.0)
