@@ -192,7 +192,7 @@ PDB_HD uint64_t sub_mod64(uint64_t a, uint64_t b, uint64_t p) { return a >= b ? 
 PDB_HD uint64_t to_mont64(uint64_t x, const Mod64& m) { return mont64(x, m.r2, m); }
 PDB_HD uint64_t from_mont64(uint64_t x, const Mod64& m) { return mont64(x, 1, m); }
 
-// (a R)^e R^-1 ... i.e. Montgomery power: aR -> a^e R
+// Montgomery power: aR -> a^e R
 PDB_HD uint64_t mont_pow64(uint64_t aR, uint64_t e, const Mod64& m) {
   uint64_t r = m.r1, b = aR;
   while (e) {

@@ -318,12 +318,9 @@ static int det64_launch(pdb_prime_ctx* ctx, Staged64 src, const int32_t* ids, in
   if (nodes == 0) return 0;
   const int slots = det64_slots(r);
   if (scratch_bytes < pdb_det_scratch_bytes_u64(r, nodes)) { set_error("det scratch too small"); return -2; }
-  int64_t need = (nodes + 127) / 128;
-  int grid = (int)(need < slots / 128 ? need : slots / 128);
   // the scratch slab is indexed by the launched slot count
   det64_kernel<<<slots / 128, 128, 0, st>>>(src, ids, r, node_lo, nodes, out, static_cast<uint64_t*>(scratch),
                                             ctx->m64, tv, tc);
-  (void)grid;
   count_launch();
   return check_launch("det64");
 }
