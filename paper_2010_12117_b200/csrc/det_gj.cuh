@@ -37,6 +37,9 @@ constexpr int GJ_B = 8;
 #ifndef PDB_GJ_MINB
 #define PDB_GJ_MINB 2   // resident 256-thread CTAs per SM the register budget is sized for
 #endif
+#ifndef PDB_GJ_MINB8
+#define PDB_GJ_MINB8 2  // the same for 8 lanes per matrix (small orders: smem is not the limit)
+#endif
 
 struct GjGeom {
   int r;    // matrix order
@@ -100,24 +103,32 @@ __device__ __forceinline__ int64_t gj_node_dft8(int64_t it, int slot, const GjGe
 
 // ---- fills: the RP x RP matrices of one iteration (padding = Montgomery identity) ----
 __device__ __forceinline__ void gj_fill(const StagedSrc& src, uint32_t* mats, const GjGeom& g, const int32_t* ids,
-                                        int64_t it, int64_t node_lo, int64_t nodes, uint32_t one) {
+                                        int64_t it, int64_t node_lo, int64_t nodes, uint32_t one, bool dense) {
   const int r = g.r, RP = g.RP, S = g.S, M = g.M;
   const int slot = threadIdx.x % M;
   const int64_t n = gj_node_linear(it, slot, g, nodes);
   if (n >= 0) {
     const uint32_t* col = src.grids + node_lo + n;
     uint32_t* dst = mats + (size_t)slot * g.MS;
-    GjPos pi(threadIdx.x / M, blockDim.x / M, RP);
-    for (; pi.i < RP; pi.next()) {
-      if (pi.i < r && pi.j < r) gj_cp_async4(dst + pi.i * S + pi.j, col + (int64_t)__ldg(ids + pi.i * r + pi.j) * src.stride);
-      else dst[pi.i * S + pi.j] = pi.i == pi.j ? one : 0u;
+    const int first = threadIdx.x / M, step = blockDim.x / M;
+    if (dense) {
+      // entry_ids[p] == p, no padding: position p is grid p and smem word p
+      const int64_t jump = (int64_t)step * src.stride;
+      const uint32_t* s0 = col + (int64_t)first * src.stride;
+      for (int q = first; q < r * r; q += step, s0 += jump) gj_cp_async4(dst + q, s0);
+    } else {
+      GjPos pi(first, step, RP);
+      for (; pi.i < RP; pi.next()) {
+        if (pi.i < r && pi.j < r) gj_cp_async4(dst + pi.i * S + pi.j, col + (int64_t)__ldg(ids + pi.i * r + pi.j) * src.stride);
+        else dst[pi.i * S + pi.j] = pi.i == pi.j ? one : 0u;
+      }
     }
   }
   gj_cp_async_wait_all();
 }
 
 __device__ __forceinline__ void gj_fill(const FusedSrc& src, uint32_t* mats, const GjGeom& g, const int32_t* ids,
-                                        int64_t it, int64_t node_lo, int64_t nodes, uint32_t one) {
+                                        int64_t it, int64_t node_lo, int64_t nodes, uint32_t one, bool) {
   const int r = g.r, RP = g.RP, S = g.S, M = g.M;
   const int slot = threadIdx.x % M;
   const int64_t n = gj_node_linear(it, slot, g, nodes);
@@ -362,7 +373,8 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
     return (float)t / (float)(passes * LPM);
   };
   // 2x8 tiles need ~70 registers: only when fewer than 4 CTAs share an SM
-  if (PDB_GJ_MINB < 4 && util(2, 8) >= 0.7f) gj_tpass<2, 8, LPM>(A, S, K, mrem, cR, l, m);
+  constexpr int minb = LPM == 8 ? PDB_GJ_MINB8 : PDB_GJ_MINB;
+  if (minb < 4 && util(2, 8) >= 0.7f) gj_tpass<2, 8, LPM>(A, S, K, mrem, cR, l, m);
   else if (util(2, 4) >= 0.7f) gj_tpass<2, 4, LPM>(A, S, K, mrem, cR, l, m);
   else if (util(1, 4) >= 0.7f) gj_tpass<1, 4, LPM>(A, S, K, mrem, cR, l, m);
   else gj_tpass<1, 2, LPM>(A, S, K, mrem, cR, l, m);
@@ -434,7 +446,7 @@ __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, in
 
 // ---- the kernel ------------------------------------------------------------------------------
 template <class Src, bool DFT8, int LPM>
-__global__ void __launch_bounds__(256, PDB_GJ_MINB)
+__global__ void __launch_bounds__(256, LPM == 8 ? PDB_GJ_MINB8 : PDB_GJ_MINB)
 det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t nodes,
               uint32_t* __restrict__ num_out, uint32_t* __restrict__ den_out,
               unsigned long long* __restrict__ flag_count, int64_t* __restrict__ flag_nodes, GjGeom g, Mod32 m) {
@@ -455,8 +467,8 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
   const int pj = l / LPR, pc = EPL * (l % LPR);   // my pivot-block row / first column
 
   const int64_t iters = DFT8 ? (nodes / g.M) : (nodes + g.M - 1) / g.M;
-  bool dense = false;
-  if constexpr (DFT8) {
+  bool dense;   // identity entry ids and no padding: affine fills
+  {
     bool id = g.RP == r && g.S == r;
     for (int e = threadIdx.x; e < r * r; e += blockDim.x) id = id && __ldg(ids + e) == e;
     dense = __syncthreads_and(id) != 0;
@@ -465,7 +477,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
   for (int64_t it = blockIdx.x; it < iters; it += gridDim.x) {
     __syncthreads();
     if constexpr (DFT8) gj_fill_dft8(src, mats, g, ids, it, node_lo, one, dense);
-    else gj_fill(src, mats, g, ids, it, node_lo, nodes, one);
+    else gj_fill(src, mats, g, ids, it, node_lo, nodes, one, dense);
     __syncthreads();
     int64_t node;
     if constexpr (DFT8) node = gj_node_dft8(it, slot, g, src.NL);
@@ -594,14 +606,14 @@ inline size_t gj_smem(const GjGeom& g) {
   return sizeof(uint32_t) * (size_t)g.M * g.MS;
 }
 
-// lanes per matrix (measured on B200, profiles/README_r01.md: 16 beats 32 and 8 at r = 40)
+// lanes per matrix (measured on B200, profiles/README_r01.md: 16 beats 32 and 8 at r = 40 and at r = 10..16)
 inline int gj_lpm(int r) {
   static const char* env = getenv("PDB_GJ_LPM");
   if (env && *env) {
     const int v = atoi(env);
     return v == 8 || v == 16 ? v : 32;
   }
-  return r > 16 ? 16 : 8;
+  return 16;
 }
 
 // warps per CTA: DFT-8 needs M % 8 == 0; otherwise as many resident matrices as fit
