@@ -33,6 +33,10 @@
 namespace pdb {
 
 constexpr int GJ_B = 8;
+// negX rows: row j at word gj_nx_row(j); rows 0-3 and 4-7 are offset by 4 words so that
+// the two row groups of the M pass fall in different shared-memory bank groups
+__host__ __device__ constexpr int gj_nx_row(int j) { return j * GJ_B + (j / 4) * 4; }
+constexpr int GJ_NX_WORDS = 8 * GJ_B + 4;
 
 #ifndef PDB_GJ_MINB
 #define PDB_GJ_MINB 2   // resident 256-thread CTAs per SM the register budget is sized for
@@ -45,7 +49,7 @@ struct GjGeom {
   int r;    // matrix order
   int RP;   // padded order, multiple of 8
   int S;    // row stride (words): multiple of 4 with S/4 odd, >= RP
-  int MS;   // matrix stride (words): RP*S + negX (64)
+  int MS;   // matrix stride (words): RP*S + negX, padded to 16 mod 32
   int M;    // matrices per CTA iteration
   int U;    // fused DFT-8 fill: distinct u per iteration (M = 8U); 0 = off
 };
@@ -322,6 +326,29 @@ __device__ __forceinline__ void gj_st(uint32_t* a, const uint32_t (&v)[TC]) {
   }
 }
 
+// TC-word row segment with its two 16-byte halves rotated by sw (0 or 4 words, TC == 8 only)
+template <int TC>
+__device__ __forceinline__ void gj_ld_sw(const uint32_t* a, int sw, uint32_t (&v)[TC]) {
+  if constexpr (TC == 8) {
+    const uint4 x = *reinterpret_cast<const uint4*>(a + sw);
+    const uint4 y = *reinterpret_cast<const uint4*>(a + (4 - sw));
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+  } else {
+    gj_ld<TC>(a, v);
+  }
+}
+
+template <int TC>
+__device__ __forceinline__ void gj_st_sw(uint32_t* a, int sw, const uint32_t (&v)[TC]) {
+  if constexpr (TC == 8) {
+    *reinterpret_cast<uint4*>(a + sw) = make_uint4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<uint4*>(a + (4 - sw)) = make_uint4(v[4], v[5], v[6], v[7]);
+  } else {
+    gj_st<TC>(a, v);
+  }
+}
+
 template <int TR, int TC, int LPM>
 __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, uint32_t cR, int l, const Mod32& m) {
   const int c0 = K + GJ_B;
@@ -332,6 +359,11 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
   const int dti = LPM / ntc, dtc = LPM - (LPM / ntc) * ntc;
   for (int w = l; w < tiles; w += LPM) {
     const int i0 = c0 + TR * ti, cc = c0 + TC * tc;
+    // 8-wide tiles: odd tile rows visit their two 16-byte chunks in swapped order,
+    // so the 8 lanes of a quarter-warp (two tile rows x four column tiles) hit 8
+    // distinct bank groups; column v of this lane's tile is physical column
+    // cc + ((v + sw) mod 8).
+    const int sw = (TC == 8 && (ti & 1)) ? 4 : 0;
     uint32_t a21[TR][GJ_B];
     uint64_t acc[TR][TC];
 #pragma unroll
@@ -339,14 +371,14 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
       const uint32_t* row = A + (i0 + a) * S;
       gj_ld<GJ_B>(row + K, a21[a]);
       uint32_t v[TC];
-      gj_ld<TC>(row + cc, v);
+      gj_ld_sw<TC>(row + cc, sw, v);
 #pragma unroll
       for (int b = 0; b < TC; ++b) acc[a][b] = mad_wide(v[b], cR, 0ull);
     }
 #pragma unroll
     for (int q = 0; q < GJ_B; ++q) {
       uint32_t nm[TC];
-      gj_ld<TC>(npr + q * S + cc, nm);
+      gj_ld_sw<TC>(npr + q * S + cc, sw, nm);
 #pragma unroll
       for (int a = 0; a < TR; ++a)
 #pragma unroll
@@ -357,7 +389,7 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
       uint32_t v[TC];
 #pragma unroll
       for (int b = 0; b < TC; ++b) v[b] = gj_red(acc[a][b], m);
-      gj_st<TC>(A + (i0 + a) * S + cc, v);
+      gj_st_sw<TC>(A + (i0 + a) * S + cc, sw, v);
     }
     ti += dti; tc += dtc;
     if (tc >= ntc) { tc -= ntc; ++ti; }
@@ -397,24 +429,18 @@ __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S,
     const int c = K + GJ_B + TC * cg;
     uint32_t res[RPI][TC];
     if (act) {
+      uint32_t x[RPI][GJ_B];   // this item's negX rows, 16 B loads
+#pragma unroll
+      for (int t = 0; t < RPI; ++t) gj_ld<GJ_B>(NX + gj_nx_row(rg * RPI + t), x[t]);
       uint64_t acc[RPI][TC];
 #pragma unroll
       for (int q = 0; q < GJ_B; ++q) {
         uint32_t a[TC];
         gj_ld<TC>(A + (K + q) * S + c, a);
-        if (q == 0) {
 #pragma unroll
-          for (int t = 0; t < RPI; ++t)
+        for (int t = 0; t < RPI; ++t)
 #pragma unroll
-            for (int b = 0; b < TC; ++b) acc[t][b] = mad_wide(NX[(rg * RPI + t) * GJ_B], a[b], 0ull);
-        } else {
-#pragma unroll
-          for (int t = 0; t < RPI; ++t) {
-            const uint32_t x = NX[(rg * RPI + t) * GJ_B + q];
-#pragma unroll
-            for (int b = 0; b < TC; ++b) acc[t][b] = mad_wide(x, a[b], acc[t][b]);
-          }
-        }
+          for (int b = 0; b < TC; ++b) acc[t][b] = mad_wide(x[t][q], a[b], q ? acc[t][b] : 0ull);
       }
 #pragma unroll
       for (int t = 0; t < RPI; ++t)
@@ -533,7 +559,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
 #pragma unroll
       for (int k = 0; k < EPL; ++k) {
         const uint32_t x = gj_mont(v[k], zl, m);
-        NX[pj * GJ_B + pc + k] = x ? p - x : 0u;
+        NX[gj_nx_row(pj) + pc + k] = x ? p - x : 0u;
       }
       __syncwarp(omask);
       // ---------------- M: negM = negX * A12, in place in the pivot rows ----------------
@@ -596,7 +622,10 @@ inline GjGeom gj_geom(int r, int warps, int lpm, bool dft8) {
   g.r = r;
   g.RP = (r + 7) & ~7;
   g.S = gj_row_stride(g.RP);
-  g.MS = g.RP * g.S + GJ_B * GJ_B;
+  // matrix stride = 16 (mod 32) words: the two matrices of a warp (and the U
+  // matrices a fill thread group writes) start in opposite bank halves
+  g.MS = g.RP * g.S + GJ_NX_WORDS;
+  g.MS += ((16 - g.MS % 32) + 32) % 32;
   g.M = warps * (32 / lpm);
   g.U = dft8 ? g.M / 8 : 0;
   return g;
