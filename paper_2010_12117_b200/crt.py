@@ -127,8 +127,8 @@ def device_lift(residues_dev, primes, n: int, stride: int) -> list:
     sel = limbs.index_select(0, idx)[:, :width].contiguous()
     sel_neg = neg.index_select(0, idx)
     host = native.host_module()
-    return host.ints_from_limbs(sel.cpu().numpy().tobytes(), idx.cpu().numpy().tobytes(),
-                                sel_neg.cpu().numpy().tobytes(), int(n), int(width))
+    return host.ints_from_limbs(np.ascontiguousarray(sel.cpu().numpy()), np.ascontiguousarray(idx.cpu().numpy()),
+                                np.ascontiguousarray(sel_neg.cpu().numpy()), int(n), int(width))
 
 
 def mrc_digits(residues, basis: CrtBasis) -> list:

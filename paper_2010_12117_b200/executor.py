@@ -132,7 +132,7 @@ class DevicePlan:
         self.staged = staged or self.vn == 0 or self.wide
         entries, coeffs = [], []
         for e, t in enumerate(m.unique_entries):
-            for exps, c in t.terms().items():
+            for exps, c in t._nonzero():
                 entries.append((e, exps))
                 coeffs.append(c)
         mag, neg, L = _limbs_of(coeffs)
