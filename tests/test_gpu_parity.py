@@ -220,6 +220,33 @@ def test_modes_agree_on_harmonic_rung(cuda, mode, monkeypatch):
     assert got == want
 
 
+@pytest.mark.parametrize("r,vn,degs,seed", [
+    (3, 2, (2, 11), 1),    # r <= 8 (register kernel) on the fused layout, E = 12 > 8: Horner fill
+    (9, 2, (3, 4), 2),     # padded order (RP = 16), DFT-8 fill, non-dense positions
+    (10, 3, (1, 1, 6), 3), # 3 variables, E = 7
+    (10, 2, (1, 2), 4),    # short last axis (N = 32): U-group divisibility edge
+])
+def test_fused_mode_edge_shapes_vs_oracle(cuda, monkeypatch, r, vn, degs, seed):
+    """The fused path (partial forward NTT + in-kernel last-axis evaluation) at
+    shapes that select each fill variant, against the oracle pipeline."""
+    import itertools
+    rng = random.Random(seed)
+    names = ("x", "y", "z")[:vn]
+
+    def entry():
+        mons = list(itertools.product(*(range(d + 1) for d in degs)))
+        return {e: rng.randint(-50, 50) for e in rng.sample(mons, min(len(mons), 6))}
+
+    rows = [[entry() for _ in range(r)] for _ in range(r)]
+    m = poly_matrix(rows, names)
+    monkeypatch.setattr(executor, "FORCE_MODE", "fused")
+    pl = plan(m)
+    got = run(m)
+    want, _ = O.run_pipeline([t.terms() for t in m.unique_entries], m.entry_ids, m.r, pl.shape,
+                             [(s.p, s.omega, s.q) for s in pl.primes])
+    assert list(got.coeffs) == want
+
+
 def test_workspace_artifacts_byte_identical_to_reference(cuda, tmp_path):
     g = golden("workspace.json")
     m = PolyMatrix.from_dict(g["input"])
