@@ -198,9 +198,11 @@ class _Timer:
 def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
     """Run the per-prime stages and the CRT (reference `_execute`, pipeline.py:323-346).
 
-    Under torch.distributed with world size G > 1 (one process per GPU), rank
-    g computes primes g, g+G, ... and the residue blocks are all-gathered
-    (NCCL) before the CRT; every rank returns the same result.
+    Under torch.distributed with world size G > 1 (one process per GPU), whole
+    rounds of G primes are prime-sharded (rank g computes primes g, g+G, ...;
+    the residue blocks are all-gathered before the CRT) and the remaining
+    P mod G primes are slab-sharded across all ranks (shard.py); every rank
+    returns the same result.
     """
     timings = StageTimings()
     if ws is not None and ws.has("crt"):
@@ -215,7 +217,8 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
     dp = DevicePlan(m, pl, device, staged)
     nodes = dp.nodes
     P = pl.prime_count
-    mine = shard.my_primes(P, rank, size)
+    whole, slab_primes = shard.split_primes(P, size) if dp.vn else (P, [])
+    mine = shard.my_primes(whole, rank, size)
     residues = torch.empty((len(mine), nodes), dtype=dp.word, device=device)
     work = torch.empty(dp.buffer_words() or 1, dtype=dp.word, device=device)
     det_chunk = nodes if dp.staged else min(nodes, FUSED_CHUNK)
@@ -242,7 +245,11 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
             ws.store_residues(unit, native.to_host_words(residues[row], dp.wide), pl.shape)
         cfg._notify(unit)
     if size > 1:
-        residues = shard.gather_residues(residues, P, rank, size)
+        residues = shard.gather_residues(residues, whole, rank, size)
+        if slab_primes:
+            slab_rows = _slab_primes(dp, slab_primes, work, det_buf, scratch, det_chunk, rank, size, cfg, events,
+                                     torch, stream)
+            residues = torch.cat([residues, slab_rows]) if whole else slab_rows
     t4 = _Timer(torch, stream).mark()
     coeffs = device_lift(residues, [s.p for s in pl.primes], nodes, nodes)
     t5 = _Timer(torch, stream).mark()
@@ -257,6 +264,46 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
         ws.store_json("crt", _payload_from_tensor(result))
     cfg._notify("crt")
     return result, timings
+
+
+def _slab_primes(dp: DevicePlan, primes, work, det_buf, scratch, chunk, rank, size, cfg, events, torch, stream):
+    """Slab-sharded primes (shard.py): every rank evaluates the entries, computes
+    the determinants of its slab of the slowest axis, all-gathers the slabs and
+    runs the inverse NTT of the full grid."""
+    pl = dp.pl
+    n0 = dp.shape[0]
+    inner = dp.nodes // n0
+    lo, hi = shard.my_slab(n0, rank, size)
+    rows = torch.empty((len(primes), dp.nodes), dtype=dp.word, device=det_buf.device)
+    for j, pi in enumerate(primes):
+        ctx = native.prime_context(pl.primes[pi], det_buf.device.index, dp.wide)
+        t0 = _Timer(torch, stream).mark()
+        _fft_stage(dp, ctx, work, None, pi, cfg)
+        t1 = _Timer(torch, stream).mark()
+        _det_range(dp, ctx, work, det_buf, scratch, chunk, lo * inner, (hi - lo) * inner)
+        full = shard.gather_slabs(det_buf[lo * inner: hi * inner], n0, inner, rank, size)
+        t2 = _Timer(torch, stream).mark()
+        rows[j].copy_(full)
+        native.ntt_multi(ctx, rows[j], 1, dp.shape, None, range(dp.vn), True)
+        t3 = _Timer(torch, stream).mark()
+        events.append((t0, t1, t2, t3))
+        cfg._notify("p%d/ifft" % pi)
+    return rows
+
+
+def _det_range(dp: DevicePlan, ctx, work, det_buf, scratch, chunk, node_lo: int, count: int):
+    """Determinants of nodes [node_lo, node_lo + count) into det_buf (same positions)."""
+    pl = dp.pl
+    if count == 0:
+        return
+    if dp.staged:
+        native.det_batch(ctx, work, dp.nodes, dp.ids, pl.r, node_lo, count, det_buf[node_lo:node_lo + count], scratch)
+        return
+    n_last = dp.shape[-1]
+    for lo in range(node_lo, node_lo + count, chunk):
+        cnt = min(chunk, node_lo + count - lo)
+        native.eval_det_fused(ctx, work, dp.outer, dp.E, dp.k, n_last, dp.ids, pl.r, lo, cnt,
+                              det_buf[lo:lo + cnt], scratch)
 
 
 def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
@@ -305,14 +352,7 @@ def _det_stage(dp: DevicePlan, ctx, work, det_buf, scratch, chunk, ws, pi, cfg):
     if ws is not None and ws.has(unit):
         det_buf.copy_(native.to_device_words(_load_grid(ws, unit, pl), dp.wide))
         return
-    if dp.staged:
-        native.det_batch(ctx, work, dp.nodes, dp.ids, pl.r, 0, dp.nodes, det_buf, scratch)
-    else:
-        n_last = dp.shape[-1]
-        for lo in range(0, dp.nodes, chunk):
-            cnt = min(chunk, dp.nodes - lo)
-            native.eval_det_fused(ctx, work, dp.outer, dp.E, dp.k, n_last, dp.ids, pl.r, lo, cnt,
-                                  det_buf[lo:lo + cnt], scratch)
+    _det_range(dp, ctx, work, det_buf, scratch, chunk, 0, dp.nodes)
     if dp.staged:   # fused mode has no det (or fft) units: it checkpoints per prime
         if ws is not None:
             ws.store_residues(unit, native.to_host_words(det_buf, dp.wide), pl.shape)

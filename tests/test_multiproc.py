@@ -67,3 +67,50 @@ def test_prime_assignment_balanced():
             parts = [shard.my_primes(P, g, G) for g in range(G)]
             assert sorted(sum(parts, [])) == list(range(P))
             assert max(map(len, parts)) - min(map(len, parts)) <= 1
+
+
+def _slab_worker(rank, size, port, case, out_path):
+    """Slab-sharded primes: each rank computes the determinants of its slab of
+    the slowest axis (oracle det on the oracle's entry grids), the slabs are
+    all-gathered and every rank interpolates the full grid."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    m = PolyMatrix.from_dict(case["input"])
+    pl = plan(m)
+    whole, slab = shard.split_primes(pl.prime_count, size)
+    n0 = pl.shape[0]
+    inner = pl.node_count // n0
+    lo, hi = shard.my_slab(n0, rank, size)
+    rows = []
+    for pi in slab:
+        spec = pl.primes[pi]
+        grids = [O.ntt_multi(O.reduce_entry(t.terms(), pl.shape, spec.p), pl.shape, spec.p, spec.omega, spec.q)
+                 for t in m.unique_entries]
+        part = O.det_grid([g[lo * inner: hi * inner] for g in grids], m.r, spec.p, m.entry_ids)
+        full = shard.gather_slabs(torch.tensor(np.asarray(part, dtype=np.int64)), n0, inner, rank, size)
+        rows.append(O.ntt_multi(full.numpy(), pl.shape, spec.p, spec.omega, spec.q, inverse=True))
+    if rank == 0:
+        np.save(out_path, np.stack(rows))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("size", [2, 3, 5])
+def test_slab_sharded_primes_match_single_process(tmp_path, size):
+    case = next(c for c in golden("runs.json") if c["name"] == "C2")
+    m = PolyMatrix.from_dict(case["input"])
+    pl = plan(m)
+    whole, slab = shard.split_primes(pl.prime_count, size)
+    assert whole + len(slab) == pl.prime_count and len(slab) == pl.prime_count % size
+    out = tmp_path / "slab.npy"
+    mp.spawn(_slab_worker, args=(size, _free_port(), case, str(out)), nprocs=size, join=True)
+    got = np.load(out)
+    assert np.array_equal(got, np.stack([_residues(m, pl, pi) for pi in slab]))
+
+
+def test_slab_partition_covers_axis():
+    for n0 in (1, 3, 16, 256):
+        for G in (1, 2, 3, 8):
+            spans = [shard.my_slab(n0, g, G) for g in range(G)]
+            assert spans[0][0] == 0 and spans[-1][1] == n0
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
