@@ -522,7 +522,6 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         for (int k = 0; k < EPL; ++k) v[k] = src_row[k];
       }
       uint32_t lam = one, zl = one, z7 = one;
-      bool zero = false;
 #pragma unroll
       for (int s = 0; s < GJ_B; ++s) {
         const uint32_t z = __shfl_sync(omask, v[s % EPL], s * LPR + s / EPL, LPM);
@@ -530,7 +529,6 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         uint32_t prow[EPL];
 #pragma unroll
         for (int k = 0; k < EPL; ++k) prow[k] = __shfl_sync(omask, v[k], s * LPR + l % LPR, LPM);
-        zero |= z == 0;
         zl = pj == s ? lam : zl;
         const uint32_t nt = p - t;   // in (0, p]: a valid multiplier for the 2-product REDC
 #pragma unroll
@@ -542,7 +540,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         if (s == GJ_B - 1) z7 = z;
         lam = gj_mont(lam, z, m);
       }
-      if (zero) { ok = false; break; }
+      if (lam == 0) { ok = false; break; }   // lam = prod z_s: zero iff a pivot vanished
       {
         // den *= lambda_1 ... lambda_6: row pj holds lambda_pj = zl; product over the rows
         uint32_t f = (pj >= 1 && pj <= 6) ? zl : one;
