@@ -11,9 +11,10 @@
 //                   complements with an 8x8 Gauss-Jordan pivot block and
 //                   delayed (64-bit accumulate + Montgomery) reduction
 //                   (det_gj.cuh).
-//  * det_robust     any r <= 64, any p < 2^31: one thread per matrix with the
-//                   reference's exact pivot rule (first nonzero column of row
-//                   i, determinant.py:136-169) and full division-free updates.
+//  * det_robust     any r <= 64, any p < 2^31: one warp per matrix (shared
+//                   memory) with the reference's exact pivot rule (first
+//                   nonzero column of row i, determinant.py:136-169) and full
+//                   division-free updates.
 //
 // The fast kernels only take diagonal pivots; a matrix whose diagonal pivot
 // vanishes is appended to a node list and recomputed by det_robust, so every
@@ -36,48 +37,72 @@ __device__ __forceinline__ void flag_node(FlagList f, int64_t node) {
 }
 
 // ---------------------------------------------------------------- robust ----
+// The reference's exact rule (determinant.py:136-169), one warp per matrix with
+// the matrix in shared memory: row i's pivot is its first nonzero column
+// (found by ballots), the rows below get the division-free update
+// z*row_k - t*row_i in parallel over (row, column) pairs, and
+// det = prod z / prod z^(r-1-i) * (-1)^(inversions of the pivot columns).
+// Any p < 2^31 (Barrett products: p = 2 and p >= 2^30 included).  Used for the
+// rare nodes whose diagonal pivot vanished in the fast kernels, and for whole
+// grids when no fast kernel applies.
+constexpr int ROBUST_WARPS = 4;
+
 template <class Src>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(32 * ROBUST_WARPS)
 det_robust(Src src, const int32_t* __restrict__ ids, int r, const int64_t* __restrict__ list,
            const unsigned long long* __restrict__ list_count, int64_t count, int64_t node_lo,
-           uint32_t* __restrict__ out, uint32_t* __restrict__ scratch, Mod32 m,
+           uint32_t* __restrict__ out, Mod32 m,
            uint32_t* __restrict__ trail_vals = nullptr, int32_t* __restrict__ trail_cols = nullptr) {
-  const int64_t slots = (int64_t)gridDim.x * blockDim.x;
-  const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  extern __shared__ uint32_t rsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* A = rsm + (size_t)warp * (r * r + r);
+  uint32_t* T = A + r * r;   // multiplier column of the current step
   const int64_t total = list ? (int64_t)*list_count : count;
   const uint32_t p = m.p;
-  uint32_t* A = scratch + slot;
-  auto at = [&](int i, int j) -> uint32_t& { return A[(int64_t)(i * r + j) * slots]; };
-  for (int64_t idx = slot; idx < total; idx += slots) {
+  const int64_t wstride = (int64_t)gridDim.x * ROBUST_WARPS;
+  for (int64_t idx = blockIdx.x * (int64_t)ROBUST_WARPS + warp; idx < total; idx += wstride) {
     const int64_t node = list ? list[idx] : node_lo + idx;
-    for (int e = 0; e < r * r; ++e) at(e / r, e % r) = src.get(ids[e], node);
+    for (int e = lane; e < r * r; e += 32) A[e] = src.get(ids[e], node) % p;
+    __syncwarp();
     uint32_t pre = 1 % p, infl = 1 % p;
     uint64_t used = 0;
     int parity = 0;
     bool alive = true;
-    for (int i = 0; i < r && alive; ++i) {
+    for (int i = 0; i < r; ++i) {
+      const uint32_t* row = A + i * r;
       int c = -1;
-      for (int j = 0; j < r; ++j)
-        if (at(i, j)) { c = j; break; }
+      for (int j0 = 0; j0 < r && c < 0; j0 += 32) {
+        const unsigned nz = __ballot_sync(0xffffffffu, j0 + lane < r && row[j0 + lane] != 0);
+        if (nz) c = j0 + __ffs(nz) - 1;
+      }
       if (c < 0) { alive = false; break; }
-      const uint32_t z = at(i, c);
-      if (trail_vals) { trail_vals[i] = z; trail_cols[i] = c; }
-      parity ^= __popcll(used >> c) & 1;   // earlier pivot columns to the right of c
+      const uint32_t z = row[c];
+      if (trail_vals && lane == 0) { trail_vals[i] = z; trail_cols[i] = c; }
+      parity ^= __popcll(used >> c) & 1;
       used |= 1ull << c;
       pre = mul_mod(pre, z, m);
       if (i + 1 < r) infl = mul_mod(infl, pre, m);
-      for (int k = i + 1; k < r; ++k) {
-        const uint32_t t = at(k, c);
-        for (int j = 0; j < r; ++j)
-          at(k, j) = sub_mod(mul_mod(z, at(k, j), m), mul_mod(t, at(i, j), m), p);
+      // rows below: (r-1-i) x r updates with the multiplier column saved first
+      const int rows = r - 1 - i;
+      for (int k = lane; k < rows; k += 32) T[k] = A[(i + 1 + k) * r + c];
+      __syncwarp();
+      const int items = rows * r;
+      for (int w = lane; w < items; w += 32) {
+        const int kk = w / r, j = w - (w / r) * r;
+        uint32_t* a = A + (i + 1 + kk) * r + j;
+        *a = sub_mod(mul_mod(z, *a, m), mul_mod(T[kk], row[j], m), p);
       }
+      __syncwarp();
     }
-    uint32_t det = 0;
-    if (alive) {
-      det = mul_mod(pre, inv_mod(infl, m), m);
-      if (parity && det) det = p - det;
+    if (lane == 0) {
+      uint32_t det = 0;
+      if (alive) {
+        det = mul_mod(pre, inv_mod(infl, m), m);
+        if (parity && det) det = p - det;
+      }
+      out[node - node_lo] = det;
     }
-    out[node - node_lo] = det;
+    __syncwarp();
   }
 }
 
@@ -160,18 +185,24 @@ static int launch_small(int r, Src src, const int32_t* ids, int64_t lo, int64_t 
   return 0;
 }
 
-int robust_slots(int r) {
-  // bounded scratch for the fallback: at most 16 Mi words of matrices
-  int64_t t = (16ll << 20) / ((int64_t)r * r);
-  if (t > 65536) t = 65536;
-  if (t < 128) t = 128;
-  return (int)(t / 128 * 128);
+size_t det_scratch_bytes(int r, int64_t nodes) {
+  (void)r;   // flag count + flagged node list + one denominator per node
+  return 256 + sizeof(int64_t) * (size_t)nodes + sizeof(uint32_t) * ((size_t)nodes + 3);
 }
 
-size_t det_scratch_bytes(int r, int64_t nodes) {
-  const size_t robust_threads = robust_slots(r);
-  return 256 + sizeof(int64_t) * (size_t)nodes + sizeof(uint32_t) * ((size_t)nodes + 3) +
-         sizeof(uint32_t) * (size_t)r * r * robust_threads;
+template <class Src>
+static void launch_robust(PrimeCtx* ctx, Src src, const int32_t* ids, int r, const int64_t* list,
+                          const unsigned long long* list_count, int64_t count, int64_t node_lo, uint32_t* out,
+                          cudaStream_t st, uint32_t* trail_vals = nullptr, int32_t* trail_cols = nullptr) {
+  const size_t smem = sizeof(uint32_t) * (size_t)ROBUST_WARPS * (r * r + r);
+  cudaFuncSetAttribute(det_robust<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // flagged lists are short (a few nodes per 10^7): one wave; whole grids: 8 CTAs per SM
+  const int64_t want = list ? (int64_t)ctx->sms : (count + ROBUST_WARPS - 1) / ROBUST_WARPS;
+  const int64_t cap = (int64_t)ctx->sms * 8;
+  const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
+  det_robust<Src><<<grid, 32 * ROBUST_WARPS, smem, st>>>(src, ids, r, list, list_count, count, node_lo, out,
+                                                         ctx->m, trail_vals, trail_cols);
+  count_launch();
 }
 
 // 2^(32 r) mod p: the Montgomery scale of an r x r determinant.
@@ -250,9 +281,7 @@ int det_run(PrimeCtx* ctx, Src src, const int32_t* ids, int r, int64_t node_lo, 
   char* base = static_cast<char*>(scratch);
   FlagList flags{reinterpret_cast<unsigned long long*>(base), reinterpret_cast<int64_t*>(base + 256)};
   uint32_t* den = reinterpret_cast<uint32_t*>(base + 256 + sizeof(int64_t) * (size_t)nodes);
-  uint32_t* mats = den + (((size_t)nodes + 3) & ~size_t(3));
   const Mod32 m = ctx->m;
-  const int slots = robust_slots(r);
   bool fast = false;
   if (cudaMemsetAsync(flags.count, 0, sizeof(unsigned long long), st) != cudaSuccess)
     return check_launch("det memset");
@@ -265,15 +294,8 @@ int det_run(PrimeCtx* ctx, Src src, const int32_t* ids, int r, int64_t node_lo, 
     if (launch_gj(ctx, r, src, ids, node_lo, nodes, out, den, flags.count, flags.nodes, st) == 0) fast = true;
   }
   if (int rc = check_launch("det fast path")) return rc;
-  if (fast) {
-    det_robust<Src><<<slots / 128, 128, 0, st>>>(src, ids, r, flags.nodes, flags.count, 0, node_lo,
-                                                  out, mats, m);
-    count_launch();
-  } else {
-    det_robust<Src><<<slots / 128, 128, 0, st>>>(src, ids, r, nullptr, nullptr, nodes, node_lo,
-                                                  out, mats, m);
-    count_launch();
-  }
+  if (fast) launch_robust(ctx, src, ids, r, flags.nodes, flags.count, 0, node_lo, out, st);
+  else launch_robust(ctx, src, ids, r, nullptr, nullptr, nodes, node_lo, out, st);
   return check_launch("det_robust");
 }
 
@@ -291,14 +313,11 @@ int condense_run(PrimeCtx* ctx, const uint32_t* mat, int r, uint32_t* trail_vals
   std::vector<int32_t> ids(r * r);
   for (int e = 0; e < r * r; ++e) ids[e] = e;
   int32_t* d_ids = static_cast<int32_t*>(scratch);
-  uint32_t* mats = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) + ((sizeof(int32_t) * r * r + 255) & ~size_t(255)));
   cudaMemcpyAsync(d_ids, ids.data(), sizeof(int32_t) * r * r, cudaMemcpyHostToDevice, st);
   cudaMemsetAsync(trail_cols, 0xff, sizeof(int32_t) * r, st);
   cudaStreamSynchronize(st);
   StagedSrc src{mat, 1};
-  det_robust<StagedSrc><<<1, 128, 0, st>>>(src, d_ids, r, nullptr, nullptr, 1, 0, det_out, mats, ctx->m,
-                                           trail_vals, trail_cols);
-  count_launch();
+  launch_robust(ctx, src, d_ids, r, nullptr, nullptr, 1, 0, det_out, st, trail_vals, trail_cols);
   return check_launch("condense");
 }
 
