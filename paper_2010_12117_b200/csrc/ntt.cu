@@ -22,61 +22,66 @@ namespace pdb {
 
 template <bool INV>
 __global__ void __launch_bounds__(256)
-ntt_axis_smem(uint32_t* __restrict__ data, AxisGeom g, int N, int logN, int TI, int LO,
+ntt_axis_smem(uint32_t* __restrict__ data, AxisGeom g, int N, int logN, int logTI, int logLO,
               const uint32_t* __restrict__ tw, const uint32_t* __restrict__ tws,
               uint32_t ninv, uint32_t ninvs, Mod32 m) {
+  // N, TI = 2^logTI inner columns and LO = 2^logLO lines per tile are powers of two:
+  // all tile index arithmetic is shifts and masks.
   extern __shared__ uint32_t sm[];
-  const int64_t tchunks = (g.inner + TI - 1) / TI;
-  const int64_t ntiles = ((g.active_outer + LO - 1) / LO) * tchunks;
-  const int tile_words = LO * N * TI;
+  __shared__ int64_t line_base[16];
+  const int TI = 1 << logTI, LO = 1 << logLO;
+  const int64_t tchunks = (g.inner + TI - 1) >> logTI;
+  const int64_t ntiles = ((g.active_outer + LO - 1) >> logLO) * tchunks;
+  const int tile_words = N << (logTI + logLO);
+  const int pairs = tile_words >> 1;
   const uint32_t p = m.p;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t oc0 = (tile / tchunks) * LO;
-    const int64_t t0 = (tile % tchunks) * TI;
-    // load (bit-reversed rows)
-    for (int w = threadIdx.x; w < tile_words; w += blockDim.x) {
-      int t = w % TI;
-      int n = (w / TI) % N;
-      int lo = w / (TI * N);
-      int64_t oc = oc0 + lo;
-      uint32_t v = 0;
-      if (oc < g.active_outer && t0 + t < g.inner) {
-        int64_t base = outer_offset(oc, g) * (int64_t)N * g.inner;
-        v = data[base + (int64_t)n * g.inner + t0 + t];
-      }
-      sm[(lo * N + bitrev(n, logN)) * TI + t] = v;
+    const int64_t oc0 = (tile / tchunks) << logLO;
+    const int64_t t0 = (tile - (tile / tchunks) * tchunks) << logTI;
+    if (threadIdx.x < LO) {
+      const int64_t oc = oc0 + threadIdx.x;
+      line_base[threadIdx.x] = oc < g.active_outer ? outer_offset(oc, g) * (int64_t)N * g.inner + t0 : -1;
     }
     __syncthreads();
-    const int pairs = LO * (N / 2) * TI;
-    for (int h = 1; h < N; h <<= 1) {
-      const int stride = N / (2 * h);
+    // load (bit-reversed rows)
+    for (int w = threadIdx.x; w < tile_words; w += blockDim.x) {
+      const int t = w & (TI - 1);
+      const int n = (w >> logTI) & (N - 1);
+      const int lo = w >> (logTI + logN);
+      const int64_t base = line_base[lo];
+      uint32_t v = 0;
+      if (base >= 0 && t0 + t < g.inner) v = data[base + (int64_t)n * g.inner + t];
+      sm[(((lo << logN) + bitrev(n, logN)) << logTI) + t] = v;
+    }
+    __syncthreads();
+    for (int lh = 0; lh < logN; ++lh) {
+      const int h = 1 << lh;
+      const int lstride = logN - 1 - lh;   // twiddle index q * N / (2h)
       for (int w = threadIdx.x; w < pairs; w += blockDim.x) {
-        int t = w % TI;
-        int j = (w / TI) % (N / 2);
-        int lo = w / (TI * (N / 2));
-        int q = j & (h - 1);
-        int a = ((j - q) << 1) + q;
-        int ia = (lo * N + a) * TI + t;
-        int ib = ia + h * TI;
-        uint32_t u = sm[ia];
-        uint32_t x = sm[ib];
-        uint32_t wv = tw[q * stride], wsv = tws[q * stride];
-        uint32_t v = shoup_mul(x, wv, wsv, p);
+        const int t = w & (TI - 1);
+        const int j = (w >> logTI) & ((N >> 1) - 1);
+        const int lo = w >> (logTI + logN - 1);
+        const int q = j & (h - 1);
+        const int a = ((j - q) << 1) + q;
+        const int ia = (((lo << logN) + a) << logTI) + t;
+        const int ib = ia + (h << logTI);
+        const uint32_t u = sm[ia];
+        const uint32_t x = sm[ib];
+        const uint32_t v = shoup_mul(x, __ldg(tw + (q << lstride)), __ldg(tws + (q << lstride)), p);
         sm[ia] = add_mod(u, v, p);
         sm[ib] = sub_mod(u, v, p);
       }
       __syncthreads();
     }
     for (int w = threadIdx.x; w < tile_words; w += blockDim.x) {
-      int t = w % TI;
-      int n = (w / TI) % N;
-      int lo = w / (TI * N);
-      int64_t oc = oc0 + lo;
-      if (oc < g.active_outer && t0 + t < g.inner) {
-        uint32_t v = sm[(lo * N + n) * TI + t];
+      const int t = w & (TI - 1);
+      const int n = (w >> logTI) & (N - 1);
+      const int lo = w >> (logTI + logN);
+      const int64_t base = line_base[lo];
+      if (base >= 0 && t0 + t < g.inner) {
+        uint32_t v = sm[(((lo << logN) + n) << logTI) + t];
         if (INV && N > 1) v = shoup_mul(v, ninv, ninvs, p);
-        int64_t base = outer_offset(oc, g) * (int64_t)N * g.inner;
-        data[base + (int64_t)n * g.inner + t0 + t] = v;
+        data[base + (int64_t)n * g.inner + t] = v;
       }
     }
     __syncthreads();
@@ -228,17 +233,20 @@ int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t
   const uint32_t* tw = inverse ? T->inv : T->fwd;
   const uint32_t* tws = inverse ? T->inv_s : T->fwd_s;
   if (N <= PDB_SMEM_NTT_MAX) {
-    int TI = (int)(g.inner < 32 ? g.inner : 32);
-    while (TI > 1 && (int64_t)N * TI > PDB_SMEM_NTT_MAX) TI >>= 1;
-    int LO = 1;
-    while ((int64_t)LO * 2 * N * TI <= 4096 && LO * 2 <= g.active_outer) LO *= 2;
-    const int64_t tiles = ((g.active_outer + LO - 1) / LO) * ((g.inner + TI - 1) / TI);
-    const size_t smem = (size_t)LO * N * TI * sizeof(uint32_t);
+    int logTI = 0;   // inner columns per tile: a power of two <= min(inner, 32)
+    while (logTI < 5 && (int64_t)2 << logTI <= g.inner && ((int64_t)N << (logTI + 1)) <= PDB_SMEM_NTT_MAX) ++logTI;
+    int logLO = 0;   // lines per tile (<= 16): fill ~4096 words
+    while (logLO < 4 && ((int64_t)N << (logTI + logLO + 1)) <= 4096 && ((int64_t)2 << logLO) <= g.active_outer)
+      ++logLO;
+    const int64_t tiles = ((g.active_outer + (1 << logLO) - 1) >> logLO) * ((g.inner + (1 << logTI) - 1) >> logTI);
+    const size_t smem = ((size_t)N << (logTI + logLO)) * sizeof(uint32_t);
     int grid = (int)(tiles < (int64_t)ctx->sms * 16 ? tiles : (int64_t)ctx->sms * 16);
     if (inverse)
-      ntt_axis_smem<true><<<grid, 256, smem, st>>>(data, g, N, logN, TI, LO, tw, tws, T->ninv, T->ninv_s, ctx->m);
+      ntt_axis_smem<true><<<grid, 256, smem, st>>>(data, g, N, logN, logTI, logLO, tw, tws, T->ninv, T->ninv_s,
+                                                    ctx->m);
     else
-      ntt_axis_smem<false><<<grid, 256, smem, st>>>(data, g, N, logN, TI, LO, tw, tws, T->ninv, T->ninv_s, ctx->m);
+      ntt_axis_smem<false><<<grid, 256, smem, st>>>(data, g, N, logN, logTI, logLO, tw, tws, T->ninv, T->ninv_s,
+                                                     ctx->m);
     count_launch();  // one launch on either branch
   } else {
     const int64_t total = g.active_outer * g.inner * (int64_t)N;
