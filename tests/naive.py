@@ -49,11 +49,21 @@ def poly_mul(a, b):
 
 
 def poly_eval(terms, point, p):
+    """sum_terms c * prod x_i^e_i mod p (power tables per coordinate)."""
+    if not terms:
+        return 0
+    tops = [max(e[i] for e in terms) for i in range(len(point))]
+    tables = []
+    for x, top in zip(point, tops):
+        row = [1 % p] * (top + 1)
+        for k in range(1, top + 1):
+            row[k] = row[k - 1] * x % p
+        tables.append(row)
     total = 0
     for exps, c in terms.items():
-        v = c
-        for x, e in zip(point, exps):
-            v = v * pow(x, e, p) % p
+        v = c % p
+        for t, e in zip(tables, exps):
+            v = v * t[e] % p
         total += v
     return total % p
 

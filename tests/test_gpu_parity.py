@@ -356,13 +356,16 @@ def test_c5_determinants_at_sampled_nodes(cuda, mode):
     del stages
 
 
-def test_schwartz_zippel_full_size_c3(cuda):
-    """Evaluate the final C3 polynomial at a random point mod a fresh prime and
-    compare with the determinant of the entry-wise evaluated matrix."""
-    m, cfg = workloads.c3()
+@pytest.mark.parametrize("config,seed", [("c3", 9), ("c5", 10)])
+def test_schwartz_zippel_full_size(cuda, config, seed):
+    """Evaluate the final polynomial (C3: 117 649 terms; C5: 4.17 M terms of up to
+    449 bits, 23 primes, the benchmark's fused path end to end) at a random point
+    mod a fresh prime and compare with the determinant of the entry-wise
+    evaluated matrix."""
+    m, cfg = getattr(workloads, config)()
     out = run(m, cfg)
     q = 2**61 - 1
-    rng = random.Random(9)
+    rng = random.Random(seed)
     point = [rng.randrange(q) for _ in range(3)]
     lhs = naive.poly_eval(out.terms(), point, q)
     mat = [[naive.poly_eval(m.entry(i, j).terms(), point, q) for j in range(m.r)] for i in range(m.r)]
