@@ -306,16 +306,31 @@ def _det_range(dp: DevicePlan, ctx, work, det_buf, scratch, chunk, node_lo: int,
                               det_buf[lo:lo + cnt], scratch)
 
 
+def _sparse_leading_axes(dp: DevicePlan) -> bool:
+    """True when ntt.cu evaluates every fused-mode leading axis with the sparse
+    kernel (forward, <= 8 nonzero rows, length >= 16; or length 1)."""
+    if os.environ.get("PDB_NTT_DENSE"):
+        return False
+    return all(n == 1 or (1 <= e <= 8 and n >= 16) for n, e in zip(dp.shape[:-1], dp.ext[:-1]))
+
+
 def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
     """Entry grids of one prime: reduce + scatter + pruned NTT (staged or partial)."""
     m, pl = dp.m, dp.pl
-    work.zero_()
     if not dp.staged:
-        native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, work)
         dims = dp.shape[:-1] + (dp.E, dp.k)
         ext = dp.ext[:-1] + [dp.E, dp.k]
+        if _sparse_leading_axes(dp):
+            # every leading axis is evaluated by the sparse kernel, which reads only
+            # the coefficient box and writes every output: zero just the box
+            box = work[: math.prod(dims)].view(dims)[tuple(slice(0, e) for e in dp.ext[:-1])]
+            box.zero_()
+        else:
+            work.zero_()
+        native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, work)
         native.ntt_multi(ctx, work, 1, dims, ext, range(dp.vn - 1), False)
         return
+    work.zero_()
     todo = []
     for eid in range(dp.k):
         unit = "p%d/fft/e%d" % (pi, eid)
