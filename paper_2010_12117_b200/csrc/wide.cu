@@ -7,9 +7,9 @@
 // test_transform.py:221-230, test_determinant.py:105-114, test_crt.py:147-153).
 // Here they are u64 residues on the GPU with Montgomery arithmetic (R = 2^64,
 // modarith.cuh:mont64); there is no CPU fallback.  These kernels are simple
-// (global-memory radix-2 NTT, one thread per matrix elimination with the
-// reference's pivot rule, one thread per coefficient CRT): the wide path is
-// for exactness at large moduli, not the throughput configuration.
+// (global-memory radix-2 NTT, one warp per matrix elimination in shared memory
+// with the reference's pivot rule, one thread per coefficient CRT): the wide
+// path is for exactness at large moduli, not the throughput configuration.
 #include <vector>
 
 #include "../../include/polydet_b200.h"
@@ -160,60 +160,68 @@ __global__ void reduce_scatter64_kernel(const uint32_t* __restrict__ mag, const 
 }
 
 // ---- determinants: the reference's exact rule (determinant.py:136-169) ------
-// One thread per matrix, entries in Montgomery form in a global scratch slab:
-// row i's pivot is its first nonzero column; rows below get the division-free
-// update z*row_k - t*row_i; det = prod z / prod z^(r-1-i) * (-1)^(inversions).
+// One warp per matrix in shared memory (Montgomery forms): row i's pivot is its
+// first nonzero column (ballots), the rows below get the division-free update
+// z*row_k - t*row_i in parallel over (row, column) pairs with the multiplier
+// column saved first; det = prod z / prod z^(r-1-i) * (-1)^(inversions).
 struct Staged64 {
   const uint64_t* grids;
   int64_t stride;
 };
 
-__global__ void __launch_bounds__(128)
+constexpr int DET64_WARPS = 4;
+
+__global__ void __launch_bounds__(32 * DET64_WARPS)
 det64_kernel(Staged64 src, const int32_t* __restrict__ ids, int r, int64_t node_lo, int64_t nodes,
-             uint64_t* __restrict__ out, uint64_t* __restrict__ scratch, Mod64 m,
-             uint64_t* __restrict__ trail_vals, int32_t* __restrict__ trail_cols) {
-  const int64_t slots = (int64_t)gridDim.x * blockDim.x;
-  const int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+             uint64_t* __restrict__ out, Mod64 m, uint64_t* __restrict__ trail_vals, int32_t* __restrict__ trail_cols) {
+  extern __shared__ uint64_t wsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* A = wsm + (size_t)warp * (r * r + r);
+  uint64_t* T = A + r * r;
   const uint64_t p = m.p;
-  uint64_t* A = scratch + slot;
-  auto at = [&](int i, int j) -> uint64_t& { return A[(int64_t)(i * r + j) * slots]; };
-  for (int64_t idx = slot; idx < nodes; idx += slots) {
+  const int64_t wstride = (int64_t)gridDim.x * DET64_WARPS;
+  for (int64_t idx = blockIdx.x * (int64_t)DET64_WARPS + warp; idx < nodes; idx += wstride) {
     const int64_t node = node_lo + idx;
-    for (int e = 0; e < r * r; ++e) at(e / r, e % r) = to_mont64(src.grids[(int64_t)ids[e] * src.stride + node], m);
+    for (int e = lane; e < r * r; e += 32) A[e] = to_mont64(src.grids[(int64_t)ids[e] * src.stride + node] % p, m);
+    __syncwarp();
     uint64_t pre = m.r1, infl = m.r1;
     uint64_t used = 0;
     int parity = 0;
     bool alive = true;
-    for (int i = 0; i < r && alive; ++i) {
+    for (int i = 0; i < r; ++i) {
+      const uint64_t* row = A + i * r;
       int c = -1;
-      for (int j = 0; j < r; ++j)
-        if (at(i, j)) { c = j; break; }
+      for (int j0 = 0; j0 < r && c < 0; j0 += 32) {
+        const unsigned nz = __ballot_sync(0xffffffffu, j0 + lane < r && row[j0 + lane] != 0);
+        if (nz) c = j0 + __ffs(nz) - 1;
+      }
       if (c < 0) { alive = false; break; }
-      const uint64_t z = at(i, c);
-      if (trail_vals) { trail_vals[i] = from_mont64(z, m); trail_cols[i] = c; }
+      const uint64_t z = row[c];
+      if (trail_vals && lane == 0) { trail_vals[i] = from_mont64(z, m); trail_cols[i] = c; }
       parity ^= __popcll(used >> c) & 1;
       used |= 1ull << c;
       pre = mont64(pre, z, m);
       if (i + 1 < r) infl = mont64(infl, pre, m);
-      for (int k = i + 1; k < r; ++k) {
-        const uint64_t t = at(k, c);
-        for (int j = 0; j < r; ++j) at(k, j) = sub_mod64(mont64(z, at(k, j), m), mont64(t, at(i, j), m), p);
+      const int rows = r - 1 - i;
+      for (int k = lane; k < rows; k += 32) T[k] = A[(i + 1 + k) * r + c];
+      __syncwarp();
+      for (int w = lane; w < rows * r; w += 32) {
+        const int kk = w / r, j = w - (w / r) * r;
+        uint64_t* a = A + (i + 1 + kk) * r + j;
+        *a = sub_mod64(mont64(z, *a, m), mont64(T[kk], row[j], m), p);
       }
+      __syncwarp();
     }
-    uint64_t det = 0;
-    if (alive) {
-      det = from_mont64(mont64(pre, mont_pow64(infl, p - 2, m), m), m);
-      if (parity && det) det = p - det;
+    if (lane == 0) {
+      uint64_t det = 0;
+      if (alive) {
+        det = from_mont64(mont64(pre, mont_pow64(infl, p - 2, m), m), m);
+        if (parity && det) det = p - det;
+      }
+      out[idx] = det;
     }
-    out[idx] = det;
+    __syncwarp();
   }
-}
-
-static int det64_slots(int r) {
-  int64_t t = (16ll << 20) / ((int64_t)r * r);
-  if (t > 65536) t = 65536;
-  if (t < 128) t = 128;
-  return (int)(t / 128 * 128);
 }
 
 // ---- CRT over up to PDB_MAX_PRIMES primes < 2^62 ------------------------------
@@ -307,20 +315,22 @@ int32_t pdb_reduce_scatter_u64(pdb_prime_ctx* ctx, const uint32_t* mag, const ui
   return check_launch("reduce_scatter64");
 }
 
-size_t pdb_det_scratch_bytes_u64(int32_t r, int64_t) {
-  return sizeof(uint64_t) * (size_t)r * r * det64_slots(r < 1 ? 1 : r) + 256;
-}
+size_t pdb_det_scratch_bytes_u64(int32_t, int64_t) { return 256; }
 
 static int det64_launch(pdb_prime_ctx* ctx, Staged64 src, const int32_t* ids, int r, int64_t node_lo, int64_t nodes,
                         uint64_t* out, void* scratch, size_t scratch_bytes, uint64_t* tv, int32_t* tc,
                         cudaStream_t st) {
+  (void)scratch;
   if (r < 1 || r > PDB_MAX_ORDER) { set_error("unsupported matrix order %d (1..%d)", r, PDB_MAX_ORDER); return -2; }
   if (nodes == 0) return 0;
-  const int slots = det64_slots(r);
   if (scratch_bytes < pdb_det_scratch_bytes_u64(r, nodes)) { set_error("det scratch too small"); return -2; }
-  // the scratch slab is indexed by the launched slot count
-  det64_kernel<<<slots / 128, 128, 0, st>>>(src, ids, r, node_lo, nodes, out, static_cast<uint64_t*>(scratch),
-                                            ctx->m64, tv, tc);
+  const size_t smem = sizeof(uint64_t) * (size_t)DET64_WARPS * (r * r + r);
+  if (cudaFuncSetAttribute(det64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return check_launch("det64 attribute");
+  const int64_t want = (nodes + DET64_WARPS - 1) / DET64_WARPS;
+  const int64_t cap = (int64_t)ctx->sms * 8;
+  const int grid = (int)(want < cap ? want : cap);
+  det64_kernel<<<grid, 32 * DET64_WARPS, smem, st>>>(src, ids, r, node_lo, nodes, out, ctx->m64, tv, tc);
   count_launch();
   return check_launch("det64");
 }
