@@ -406,7 +406,10 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
   };
   // 2x8 tiles need ~70 registers: only when fewer than 4 CTAs share an SM
   constexpr int minb = LPM == 8 ? PDB_GJ_MINB8 : PDB_GJ_MINB;
-  if (minb < 4 && util(2, 8) >= 0.7f) gj_tpass<2, 8, LPM>(A, S, K, mrem, cR, l, m);
+#ifndef PDB_GJ_T28
+#define PDB_GJ_T28 0   // 2x8 trailing tiles: more reuse but spills at 128 registers (measured slower)
+#endif
+  if (PDB_GJ_T28 && minb < 4 && util(2, 8) >= 0.7f) gj_tpass<2, 8, LPM>(A, S, K, mrem, cR, l, m);
   else if (util(2, 4) >= 0.7f) gj_tpass<2, 4, LPM>(A, S, K, mrem, cR, l, m);
   else if (util(1, 4) >= 0.7f) gj_tpass<1, 4, LPM>(A, S, K, mrem, cR, l, m);
   else gj_tpass<1, 2, LPM>(A, S, K, mrem, cR, l, m);
