@@ -249,7 +249,10 @@ __device__ __forceinline__ void gj_fill_dft8_dense(const FusedSrc& src, uint32_t
   uint32_t* base = mats + uu * g.MS;
   const uint32_t* slab = src.part + o * (int64_t)E * k;
   const int step = blockDim.x / U;
-  constexpr int F = 4;   // positions in flight
+#ifndef PDB_GJ_FILLF
+#define PDB_GJ_FILLF 4
+#endif
+  constexpr int F = PDB_GJ_FILLF;   // positions in flight
   for (int p0 = threadIdx.x / U; p0 < n; p0 += F * step) {
     uint32_t c[F][E];
 #pragma unroll
@@ -465,7 +468,10 @@ __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, in
     const int t = (mrem / tc) * (GJ_B / rpi);
     return (float)t / (float)(((t + LPM - 1) / LPM) * LPM);
   };
-  if (util(4, 4) >= 0.74f) gj_mpass<4, 4, LPM>(A, NX, S, K, mrem, l, omask, m);
+#ifndef PDB_GJ_M44
+#define PDB_GJ_M44 0   // 4x4 M-pass tiles (measured slower than 2x4 at 128 registers)
+#endif
+  if (PDB_GJ_M44 && util(4, 4) >= 0.74f) gj_mpass<4, 4, LPM>(A, NX, S, K, mrem, l, omask, m);
   else if (util(2, 4) >= 0.74f) gj_mpass<2, 4, LPM>(A, NX, S, K, mrem, l, omask, m);
   else if (util(4, 2) >= 0.74f) gj_mpass<4, 2, LPM>(A, NX, S, K, mrem, l, omask, m);
   else if (util(1, 4) >= 0.74f) gj_mpass<1, 4, LPM>(A, NX, S, K, mrem, l, omask, m);
