@@ -402,3 +402,21 @@ def test_predict_on_real_matrix(cuda):
     assert forecast.mean_rounded == Decimal(repr(mean)).quantize(Decimal("0.01"))
     with pytest.raises(ValueError):
         predict(m, pl, 0)
+
+
+def test_integration_ctypes_stub_runs(cuda):
+    """The Option B ctypes stub printed in INTEGRATION.md (a maintainer's
+    reference-side binding of pdb_det_batch_u32) runs as written and agrees
+    with the oracle."""
+    import re
+    from pathlib import Path
+    from paper_2010_12117_b200 import native
+    text = (Path(__file__).resolve().parent.parent / "INTEGRATION.md").read_text()
+    block = re.search(r"## Option B.*?```python\n(.*?)```", text, re.S).group(1)
+    block = block.replace('ctypes.CDLL("libpolydet_b200.so")', "ctypes.CDLL(%r)" % str(native.LIB_PATH))
+    env = {}
+    exec(compile(block, "INTEGRATION.md", "exec"), env)
+    spec = find_fourier_primes(8, 1, start=10**9, min_count=1)[0]
+    rng = np.random.default_rng(11)
+    grids = [rng.integers(0, spec.p, 300) for _ in range(144)]
+    assert env["det_grid"](grids, 12, spec).tolist() == O.det_grid(grids, 12, spec.p).tolist()
