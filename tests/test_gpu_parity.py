@@ -143,13 +143,15 @@ def test_det_random_vs_oracle_with_zero_pivots(cuda, r):
     assert got.tolist() == O.det_grid(grids, r, spec.p).tolist()
 
 
-@pytest.mark.parametrize("p", [2, 3, 5, 97, 65537])
+@pytest.mark.parametrize("p", [2, 3, 5, 97, 65537, 1073741789, 1073741827])
 def test_det_tiny_and_small_primes(cuda, p):
     """Even p has no Montgomery form: such primes take the robust kernel; odd
-    small primes exercise zero pivots on the fast paths constantly."""
+    small primes exercise zero pivots on the fast paths constantly;
+    1073741789 (largest prime < 2^30) is the worst case of the fast kernels'
+    accumulator bounds, 1073741827 (> 2^30) takes the robust path."""
     spec = PrimeSpec(p, p - 1, 0, 1)
-    rng = np.random.default_rng(p)
-    for r in (3, 8, 10, 24):
+    rng = np.random.default_rng(p % 1000)
+    for r in (3, 8, 10, 24, 40):
         mats = rng.integers(0, p, (300, r, r))
         grids = [mats[:, e // r, e % r] for e in range(r * r)]
         assert det_grid(grids, r, spec).tolist() == O.det_grid(grids, r, p).tolist(), (p, r)
