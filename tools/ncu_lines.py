@@ -61,7 +61,7 @@ def num(x):
 def main():
     rep, obj = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-    want = sys.argv[4].split(",") if len(sys.argv) > 4 else ["det_octet"]
+    want = sys.argv[4].split(",") if len(sys.argv) > 4 else ["det_gj_kernel", "FusedSrc"]
     kernel, rows = ncu_rows(rep)
     funcs, cands = line_map(obj, want)
     if not cands:
