@@ -16,11 +16,12 @@ from pathlib import Path
 import numpy as np
 
 from .errors import DeviceError
+from .fields import MODULUS_LIMIT, U32_KERNEL_MODULUS
 
 LIB_NAME = "libpolydet_b200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
-U32_LIMIT = 2**31   # u32 kernels: p < 2^31
-WIDE_LIMIT = 2**62  # u64 kernels (the wide path): p < 2^62
+U32_LIMIT = U32_KERNEL_MODULUS   # u32 kernels: p < 2^31
+WIDE_LIMIT = MODULUS_LIMIT       # u64 kernels (the wide path): p < 2^62
 
 
 def needs_wide(p: int) -> bool:
