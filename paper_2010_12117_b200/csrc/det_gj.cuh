@@ -99,8 +99,10 @@ __device__ __forceinline__ int64_t gj_node_linear(int64_t it, int slot, const Gj
 
 __device__ __forceinline__ int64_t gj_node_dft8(int64_t it, int slot, const GjGeom& g, int NL) {
   const int per_o = NL / (8 * g.U);
-  const int64_t o = it / per_o;
-  const int ublk = (int)(it - o * per_o);
+  // per_o = NL / (8U) is a power of two whenever the DFT-8 fill is on (8U | NL, NL = 2^k)
+  const int lpo = __ffs(per_o) - 1;
+  const int64_t o = it >> lpo;
+  const int ublk = (int)(it & (per_o - 1));
   const int v = slot / g.U, uu = slot - v * g.U;
   return o * NL + ublk * g.U + uu + (int64_t)(NL / 8) * v;
 }
@@ -154,8 +156,9 @@ __device__ __forceinline__ void gj_fill_dft8_e(const FusedSrc& src, uint32_t* ma
   const int r = g.r, RP = g.RP, S = g.S, U = g.U, NL = src.NL, k = src.k;
   const uint32_t p = src.p;
   const int per_o = NL / (8 * U);
-  const int64_t o = (node_lo / NL) + it / per_o;
-  const int ublk = (int)(it % per_o);
+  const int lpo = __ffs(per_o) - 1;   // per_o and NL are powers of two on this path
+  const int64_t o = (node_lo >> (__ffs(NL) - 1)) + (it >> lpo);
+  const int ublk = (int)(it & (per_o - 1));
   const int step8 = NL / 8;
   uint32_t w[4], ws[4];
 #pragma unroll
@@ -225,8 +228,9 @@ __device__ __forceinline__ void gj_fill_dft8_dense(const FusedSrc& src, uint32_t
   const int U = g.U, NL = src.NL, k = src.k, n = g.r * g.r;
   const uint32_t p = src.p;
   const int per_o = NL / (8 * U);
-  const int64_t o = (node_lo / NL) + it / per_o;
-  const int ublk = (int)(it % per_o);
+  const int lpo = __ffs(per_o) - 1;   // per_o and NL are powers of two on this path
+  const int64_t o = (node_lo >> (__ffs(NL) - 1)) + (it >> lpo);
+  const int ublk = (int)(it & (per_o - 1));
   const int step8 = NL / 8;
   uint32_t w[4], ws[4];
 #pragma unroll
