@@ -26,6 +26,12 @@
 //
 // A zero pivot (prob. ~r/p per node) diverts the node to det_robust, which
 // applies the reference's first-nonzero pivoting (determinant.py:136-169).
+//
+// Shape choices measured on B200 (profiles/README_r01.md): 16 lanes per matrix
+// (two matrices per warp), 8 warps per CTA, 2 CTAs per SM (shared memory holds
+// 32 matrices of 40x40); 2x4 register tiles in the M and T passes (larger tiles
+// spill at the 128-register budget); matrix stride 16 (mod 32) words and
+// swizzled 8-word tiles against bank conflicts.
 #pragma once
 #include "pdb_internal.cuh"
 #include "dft8.cuh"
@@ -48,7 +54,7 @@ constexpr int GJ_NX_WORDS = 8 * GJ_B + 4;
 struct GjGeom {
   int r;    // matrix order
   int RP;   // padded order, multiple of 8
-  int S;    // row stride (words): multiple of 4 with S/4 odd, >= RP
+  int S;    // row stride (words): RP + PDB_GJ_ROWPAD, a multiple of 4
   int MS;   // matrix stride (words): RP*S + negX, padded to 16 mod 32
   int M;    // matrices per CTA iteration
   int U;    // fused DFT-8 fill: distinct u per iteration (M = 8U); 0 = off
