@@ -1,0 +1,29 @@
+"""Small runs of every kernel family for compute-sanitizer (memcheck / racecheck /
+synccheck):  compute-sanitizer --tool racecheck python tools/sanitize.py"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import numpy as np  # noqa: E402
+
+from paper_2010_12117_b200 import (PipelineConfig, PrimeSpec, det_grid, executor, find_fourier_primes,  # noqa: E402
+                                   run, workloads)
+
+spec = find_fourier_primes(8, 1, start=10**9, min_count=1)[0]
+rng = np.random.default_rng(0)
+for r in (4, 10, 16, 40):
+    grids = [rng.integers(0, spec.p, 40) for _ in range(r * r)]
+    grids[0][::3] = 0                         # zero pivots -> robust path
+    det_grid(grids, r, spec)
+det_grid([rng.integers(0, 97, 40) for _ in range(100)], 10, PrimeSpec(97, 96, 0, 1))
+m, cfg = workloads.harmonic(3, (5, 7), True)
+executor.FORCE_MODE = "fused"
+run(m, cfg)
+executor.FORCE_MODE = "staged"
+run(m, cfg)
+executor.FORCE_MODE = None
+run(*workloads.c1())
+m = workloads.c1()[0]
+run(m, PipelineConfig(prime_start=2**61))    # wide path
+print("sanitize workload done")
