@@ -369,13 +369,15 @@ def run_ours(args):
     hbm, hbm_kind = measured_peaks()
     from paper_2010_12117_b200.executor import FUSED_CHUNK
     launch_nodes = min(nodes, FUSED_CHUNK)
-    traffic = traffic_note = None
+    traffic = traffic_note = ncu_summary = None
     tpath = ROOT / "profiles" / "ncu" / "det_traffic_r01.json"
     if tpath.exists() and args.config == "c5":
         t = json.loads(tpath.read_text())
         traffic = t["dram_bytes_per_node"] * launch_nodes
         traffic_note = ("dram read+write bytes per launch of %d nodes, scaled from %s (%d-node launch)"
                         % (launch_nodes, t["source"], t["nodes_per_launch"]))
+        ncu_summary = {k: t[k] for k in ("pipes_pct_of_peak", "issue_active_pct", "warp_instructions_per_det",
+                                          "dram_bytes_per_node", "source") if k in t}
     out = {
         "metric": "mod-p %dx%d dets/sec (%s)" % (r, r, args.config.upper()),
         "value": value, "unit": "dets/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -394,7 +396,8 @@ def run_ours(args):
                      "peak_kind": "measured now: delayed 64-bit MAC + REDC primitive (pdb_mulmod_peak v1)",
                      "shoup_peak": peak_shoup / 1e9, "frac_vs_shoup_peak": achieved / peak_shoup,
                      "det_ms_per_step": det_ms / args.steps, "det_share": det_ms / ms,
-                     "work_per_matrix": W, "hbm_peak_gbs": hbm, "hbm_peak_kind": hbm_kind},
+                     "work_per_matrix": W, "hbm_peak_gbs": hbm, "hbm_peak_kind": hbm_kind,
+                     "ncu": ncu_summary},
         "clocks": clocks,
         "gpu_launches": launches,
     }
