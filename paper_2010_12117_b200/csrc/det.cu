@@ -45,7 +45,7 @@ __device__ __forceinline__ void flag_node(FlagList f, int64_t node) {
 // Any p < 2^31 (Barrett products: p = 2 and p >= 2^30 included).  Used for the
 // rare nodes whose diagonal pivot vanished in the fast kernels, and for whole
 // grids when no fast kernel applies.
-constexpr int ROBUST_WARPS = 4;
+constexpr int ROBUST_WARPS = 4;   // most warps per CTA (fewer for large orders: smem)
 
 template <class Src>
 __global__ void __launch_bounds__(32 * ROBUST_WARPS)
@@ -59,13 +59,14 @@ det_robust(Src src, const int32_t* __restrict__ ids, int r, const int64_t* __res
   uint32_t* T = A + r * r;   // multiplier column of the current step
   const int64_t total = list ? (int64_t)*list_count : count;
   const uint32_t p = m.p;
-  const int64_t wstride = (int64_t)gridDim.x * ROBUST_WARPS;
-  for (int64_t idx = blockIdx.x * (int64_t)ROBUST_WARPS + warp; idx < total; idx += wstride) {
+  const int wpc = blockDim.x >> 5;
+  const int64_t wstride = (int64_t)gridDim.x * wpc;
+  for (int64_t idx = blockIdx.x * (int64_t)wpc + warp; idx < total; idx += wstride) {
     const int64_t node = list ? list[idx] : node_lo + idx;
     for (int e = lane; e < r * r; e += 32) A[e] = src.get(ids[e], node) % p;
     __syncwarp();
     uint32_t pre = 1 % p, infl = 1 % p;
-    uint64_t used = 0;
+    uint64_t used0 = 0, used1 = 0;   // pivot columns so far (r <= 128)
     int parity = 0;
     bool alive = true;
     for (int i = 0; i < r; ++i) {
@@ -78,8 +79,10 @@ det_robust(Src src, const int32_t* __restrict__ ids, int r, const int64_t* __res
       if (c < 0) { alive = false; break; }
       const uint32_t z = row[c];
       if (trail_vals && lane == 0) { trail_vals[i] = z; trail_cols[i] = c; }
-      parity ^= __popcll(used >> c) & 1;
-      used |= 1ull << c;
+      // earlier pivot columns to the right of c flip the permutation sign
+      parity ^= (c < 64 ? __popcll(used0 >> c) + __popcll(used1) : __popcll(used1 >> (c - 64))) & 1;
+      if (c < 64) used0 |= 1ull << c;
+      else used1 |= 1ull << (c - 64);
       pre = mul_mod(pre, z, m);
       if (i + 1 < r) infl = mul_mod(infl, pre, m);
       // rows below: (r-1-i) x r updates with the multiplier column saved first
@@ -194,14 +197,17 @@ template <class Src>
 static void launch_robust(PrimeCtx* ctx, Src src, const int32_t* ids, int r, const int64_t* list,
                           const unsigned long long* list_count, int64_t count, int64_t node_lo, uint32_t* out,
                           cudaStream_t st, uint32_t* trail_vals = nullptr, int32_t* trail_cols = nullptr) {
-  const size_t smem = sizeof(uint32_t) * (size_t)ROBUST_WARPS * (r * r + r);
+  const size_t per_warp = sizeof(uint32_t) * (size_t)(r * r + r);
+  int warps = (int)((200u * 1024u) / per_warp);
+  warps = warps < 1 ? 1 : (warps > ROBUST_WARPS ? ROBUST_WARPS : warps);
+  const size_t smem = per_warp * warps;
   cudaFuncSetAttribute(det_robust<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // flagged lists are short (a few nodes per 10^7): one wave; whole grids: 8 CTAs per SM
-  const int64_t want = list ? (int64_t)ctx->sms : (count + ROBUST_WARPS - 1) / ROBUST_WARPS;
+  const int64_t want = list ? (int64_t)ctx->sms : (count + warps - 1) / warps;
   const int64_t cap = (int64_t)ctx->sms * 8;
   const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
-  det_robust<Src><<<grid, 32 * ROBUST_WARPS, smem, st>>>(src, ids, r, list, list_count, count, node_lo, out,
-                                                         ctx->m, trail_vals, trail_cols);
+  det_robust<Src><<<grid, 32 * warps, smem, st>>>(src, ids, r, list, list_count, count, node_lo, out,
+                                                  ctx->m, trail_vals, trail_cols);
   count_launch();
 }
 

@@ -179,13 +179,14 @@ det64_kernel(Staged64 src, const int32_t* __restrict__ ids, int r, int64_t node_
   uint64_t* A = wsm + (size_t)warp * (r * r + r);
   uint64_t* T = A + r * r;
   const uint64_t p = m.p;
-  const int64_t wstride = (int64_t)gridDim.x * DET64_WARPS;
-  for (int64_t idx = blockIdx.x * (int64_t)DET64_WARPS + warp; idx < nodes; idx += wstride) {
+  const int wpc = blockDim.x >> 5;
+  const int64_t wstride = (int64_t)gridDim.x * wpc;
+  for (int64_t idx = blockIdx.x * (int64_t)wpc + warp; idx < nodes; idx += wstride) {
     const int64_t node = node_lo + idx;
     for (int e = lane; e < r * r; e += 32) A[e] = to_mont64(src.grids[(int64_t)ids[e] * src.stride + node] % p, m);
     __syncwarp();
     uint64_t pre = m.r1, infl = m.r1;
-    uint64_t used = 0;
+    uint64_t used0 = 0, used1 = 0;   // pivot columns so far (r <= 128)
     int parity = 0;
     bool alive = true;
     for (int i = 0; i < r; ++i) {
@@ -198,8 +199,10 @@ det64_kernel(Staged64 src, const int32_t* __restrict__ ids, int r, int64_t node_
       if (c < 0) { alive = false; break; }
       const uint64_t z = row[c];
       if (trail_vals && lane == 0) { trail_vals[i] = from_mont64(z, m); trail_cols[i] = c; }
-      parity ^= __popcll(used >> c) & 1;
-      used |= 1ull << c;
+      // earlier pivot columns to the right of c flip the permutation sign
+      parity ^= (c < 64 ? __popcll(used0 >> c) + __popcll(used1) : __popcll(used1 >> (c - 64))) & 1;
+      if (c < 64) used0 |= 1ull << c;
+      else used1 |= 1ull << (c - 64);
       pre = mont64(pre, z, m);
       if (i + 1 < r) infl = mont64(infl, pre, m);
       const int rows = r - 1 - i;
@@ -324,13 +327,16 @@ static int det64_launch(pdb_prime_ctx* ctx, Staged64 src, const int32_t* ids, in
   if (r < 1 || r > PDB_MAX_ORDER) { set_error("unsupported matrix order %d (1..%d)", r, PDB_MAX_ORDER); return -2; }
   if (nodes == 0) return 0;
   if (scratch_bytes < pdb_det_scratch_bytes_u64(r, nodes)) { set_error("det scratch too small"); return -2; }
-  const size_t smem = sizeof(uint64_t) * (size_t)DET64_WARPS * (r * r + r);
+  const size_t per_warp = sizeof(uint64_t) * (size_t)(r * r + r);
+  int warps = (int)((200u * 1024u) / per_warp);
+  warps = warps < 1 ? 1 : (warps > DET64_WARPS ? DET64_WARPS : warps);
+  const size_t smem = per_warp * warps;
   if (cudaFuncSetAttribute(det64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return check_launch("det64 attribute");
-  const int64_t want = (nodes + DET64_WARPS - 1) / DET64_WARPS;
+  const int64_t want = (nodes + warps - 1) / warps;
   const int64_t cap = (int64_t)ctx->sms * 8;
   const int grid = (int)(want < cap ? want : cap);
-  det64_kernel<<<grid, 32 * DET64_WARPS, smem, st>>>(src, ids, r, node_lo, nodes, out, ctx->m64, tv, tc);
+  det64_kernel<<<grid, 32 * warps, smem, st>>>(src, ids, r, node_lo, nodes, out, ctx->m64, tv, tc);
   count_launch();
   return check_launch("det64");
 }
