@@ -6,12 +6,12 @@
 //
 //  * det_small<R>   R <= 8: one lane per matrix, the matrix in registers,
 //                   division-free elimination with diagonal pivots.
-//  * det_gj         9 <= r <= 64 and odd p < 2^30: a lane group (8/16/32
+//  * det_gj         9 <= r <= 128 and odd p < 2^30: a lane group (8/16/32
 //                   lanes) per matrix in shared memory, blocked Schur
 //                   complements with an 8x8 Gauss-Jordan pivot block and
 //                   delayed (64-bit accumulate + Montgomery) reduction
 //                   (det_gj.cuh).
-//  * det_robust     any r <= 64, any p < 2^31: one warp per matrix (shared
+//  * det_robust     any r <= 128, any p < 2^31: one warp per matrix (shared
 //                   memory) with the reference's exact pivot rule (first
 //                   nonzero column of row i, determinant.py:136-169) and full
 //                   division-free updates.
