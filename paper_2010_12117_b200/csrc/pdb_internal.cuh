@@ -7,7 +7,7 @@
 
 #include "modarith.cuh"
 
-#define PDB_MAX_DIMS 8
+#define PDB_MAX_DIMS 16
 #define PDB_SMEM_NTT_MAX 8192   // longest axis transformed in shared memory
 #define PDB_MAX_ORDER 128       // largest matrix order r
 #define PDB_MAX_PRIMES 256      // most primes in one CRT call

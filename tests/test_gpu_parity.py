@@ -422,3 +422,25 @@ def test_integration_ctypes_stub_runs(cuda):
     rng = np.random.default_rng(11)
     grids = [rng.integers(0, spec.p, 300) for _ in range(144)]
     assert env["det_grid"](grids, 12, spec).tolist() == O.det_grid(grids, 12, spec.p).tolist()
+
+
+@pytest.mark.parametrize("mode", ["staged", "fused"])
+def test_many_variables_vs_oracle(cuda, monkeypatch, mode):
+    """Nine variables (grid 4^9 = 262 144 nodes): NTTs over nine axes, fused
+    layout with eleven dimensions."""
+    rng = random.Random(99)
+    nv = 9
+    names = tuple("v%d" % i for i in range(nv))
+
+    def entry():
+        return {tuple(int(i == a) for i in range(nv)): rng.randint(-5, 5) for a in rng.sample(range(nv), 3)}
+
+    rows = [[entry() for _ in range(3)] for _ in range(3)]
+    m = poly_matrix(rows, names)
+    monkeypatch.setattr(executor, "FORCE_MODE", mode)
+    pl = plan(m)
+    got = run(m)
+    want, _ = O.run_pipeline([t.terms() for t in m.unique_entries], m.entry_ids, m.r, pl.shape,
+                             [(s.p, s.omega, s.q) for s in pl.primes])
+    assert list(got.coeffs) == want
+    assert got.terms() == naive.symbolic_det(rows, nv)
