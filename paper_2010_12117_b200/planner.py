@@ -28,11 +28,11 @@ from .layout import PolyMatrix, pad_shape
 class PipelineConfig:
     """Planning and scheduling knobs (reference `pipeline.py:45-63`).
 
-    `workers` and `chunk_size` are accepted for drop-in compatibility; on the
-    GPU they never change results (like the reference) and only `chunk_size`
-    is used, as an upper bound on nodes per determinant launch.
-    `devices` > 1 shards primes across GPUs (one process per GPU under
-    torch.distributed; see executor.py).
+    `workers` and `chunk_size` are accepted for drop-in compatibility; like in
+    the reference they never change results, and on the GPU they are not
+    used (the device kernels size their own launches).  Multi-GPU runs shard
+    primes across the processes of a torch.distributed job (one per GPU; see
+    executor.py and shard.py), not through this config.
     """
 
     prime_start: int = 10**9
@@ -41,7 +41,6 @@ class PipelineConfig:
     workers: int = 1
     chunk_size: int = 4096
     progress: Optional[Callable[[str], None]] = None
-    devices: int = 1
 
     def _notify(self, unit: str):
         if self.progress is not None:
