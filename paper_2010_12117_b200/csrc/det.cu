@@ -221,23 +221,23 @@ static uint32_t mont_scale(const Mod32& m, int r) {
   return (uint32_t)acc;
 }
 
-template <class Src, bool DFT8, int LPM>
+template <class Src, bool DFT8, int LPM, bool P31>
 static int launch_gj_geom(PrimeCtx* ctx, const GjGeom& g, Src src, const int32_t* ids, int64_t node_lo,
                           int64_t nodes, uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn,
                           cudaStream_t st) {
   const size_t smem = gj_smem(g);
-  if (cudaFuncSetAttribute(det_gj_kernel<Src, DFT8, LPM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(det_gj_kernel<Src, DFT8, LPM, P31>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return check_launch("det_gj attribute");
   int ctas_per_sm = 0;
   const int threads = g.M * LPM;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, det_gj_kernel<Src, DFT8, LPM>, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, det_gj_kernel<Src, DFT8, LPM, P31>, threads, smem);
   if (ctas_per_sm < 1) ctas_per_sm = 1;
   const int64_t iters = DFT8 ? nodes / g.M : (nodes + g.M - 1) / g.M;
   const int64_t cap = (int64_t)ctx->sms * ctas_per_sm;
   const int grid = (int)(iters < cap ? iters : cap);
   if (grid < 1) return 0;
-  det_gj_kernel<Src, DFT8, LPM><<<grid, threads, smem, st>>>(src, ids, node_lo, nodes, out, den, fc, fn, g, ctx->m);
+  det_gj_kernel<Src, DFT8, LPM, P31><<<grid, threads, smem, st>>>(src, ids, node_lo, nodes, out, den, fc, fn, g, ctx->m);
   count_launch();
   if (int rc = check_launch("det_gj")) return rc;
   const int64_t fblocks = (nodes + 255) / 256;
@@ -248,28 +248,27 @@ static int launch_gj_geom(PrimeCtx* ctx, const GjGeom& g, Src src, const int32_t
 }
 
 template <class Src, bool DFT8>
-static int launch_gj_lpm(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int64_t node_lo, int64_t nodes,
+static int launch_gj_mode(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int64_t node_lo, int64_t nodes,
                          uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
-  const int lpm = gj_lpm(r);
-  if (lpm == 32)
-    return launch_gj_geom<Src, DFT8, 32>(ctx, gj_pick(r, 32, DFT8), src, ids, node_lo, nodes, out, den, fc, fn, st);
-  if (lpm == 16)
-    return launch_gj_geom<Src, DFT8, 16>(ctx, gj_pick(r, 16, DFT8), src, ids, node_lo, nodes, out, den, fc, fn, st);
-  return launch_gj_geom<Src, DFT8, 8>(ctx, gj_pick(r, 8, DFT8), src, ids, node_lo, nodes, out, den, fc, fn, st);
+  // 16 lanes per matrix (the measured best for every order); 2^30 <= p < 2^31 reduces pairs of products
+  const GjGeom g = gj_pick(r, 16, DFT8);
+  if (ctx->m.fast())
+    return launch_gj_geom<Src, DFT8, 16, false>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+  return launch_gj_geom<Src, DFT8, 16, true>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
 }
 
 static int launch_gj(PrimeCtx* ctx, int r, StagedSrc src, const int32_t* ids, int64_t node_lo, int64_t nodes,
                      uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
-  return launch_gj_lpm<StagedSrc, false>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
+  return launch_gj_mode<StagedSrc, false>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
 }
 
 static int launch_gj(PrimeCtx* ctx, int r, FusedSrc src, const int32_t* ids, int64_t node_lo, int64_t nodes,
                      uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
-  const GjGeom g = gj_pick(r, gj_lpm(r), true);
+  const GjGeom g = gj_pick(r, 16, true);
   const bool dft8 = src.E <= 8 && src.NL >= 8 && src.NL % (8 * g.U) == 0 && node_lo % src.NL == 0 &&
                     nodes % src.NL == 0;
-  if (dft8) return launch_gj_lpm<FusedSrc, true>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
-  return launch_gj_lpm<FusedSrc, false>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
+  if (dft8) return launch_gj_mode<FusedSrc, true>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
+  return launch_gj_mode<FusedSrc, false>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
 }
 
 template <class Src>
@@ -296,7 +295,7 @@ int det_run(PrimeCtx* ctx, Src src, const int32_t* ids, int r, int64_t node_lo, 
     int grid = (int)(blocks < (int64_t)ctx->sms * 32 ? blocks : (int64_t)ctx->sms * 32);
     launch_small(r, src, ids, node_lo, nodes, out, flags, m, grid, st);
     fast = true;
-  } else if (m.fast()) {
+  } else if (m.odd() && m.p < (1u << 31)) {   // det_gj: p < 2^30 fast mode, [2^30, 2^31) paired mode
     if (launch_gj(ctx, r, src, ids, node_lo, nodes, out, den, flags.count, flags.nodes, st) == 0) fast = true;
   }
   if (int rc = check_launch("det fast path")) return rc;

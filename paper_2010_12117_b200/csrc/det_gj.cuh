@@ -22,7 +22,9 @@
 // does the single modular inversion per node (batched by 32 per warp).
 // Accumulators hold <= 9 products of canonical residues: 9 p^2 < 2^63.2 for
 // p < 2^30 (Mod32::fast), inside REDC's bound; REDC output < 3.25 p is made
-// canonical with two conditional subtractions (ALU pipe, no IMAD.HI).
+// canonical with two conditional subtractions (ALU pipe, no IMAD.HI).  For
+// 2^30 <= p < 2^31 (template P31) the M and T passes reduce every two
+// products and add the partial results mod p.
 //
 // A zero pivot (prob. ~r/p per node) diverts the node to det_robust, which
 // applies the reference's first-nonzero pivoting (determinant.py:136-169).
@@ -46,9 +48,6 @@ constexpr int GJ_NX_WORDS = 8 * GJ_B + 4;
 
 #ifndef PDB_GJ_MINB
 #define PDB_GJ_MINB 2   // resident 256-thread CTAs per SM the register budget is sized for
-#endif
-#ifndef PDB_GJ_MINB8
-#define PDB_GJ_MINB8 2  // the same for 8 lanes per matrix (small orders: smem is not the limit)
 #endif
 
 struct GjGeom {
@@ -362,7 +361,9 @@ __device__ __forceinline__ void gj_st_sw(uint32_t* a, int sw, const uint32_t (&v
   }
 }
 
-template <int TR, int TC, int LPM>
+// P31: 2^30 <= p < 2^31 -- at most two products per reduction (2 p^2 < 2^63 keeps
+// hi(acc) + p < 2^32); the partial results are summed mod p.
+template <int TR, int TC, int LPM, bool P31>
 __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, uint32_t cR, int l, const Mod32& m) {
   const int c0 = K + GJ_B;
   const int ntc = mrem / TC;
@@ -388,6 +389,7 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
 #pragma unroll
       for (int b = 0; b < TC; ++b) acc[a][b] = mad_wide(v[b], cR, 0ull);
     }
+    uint32_t sum[TR][TC];
 #pragma unroll
     for (int q = 0; q < GJ_B; ++q) {
       uint32_t nm[TC];
@@ -395,13 +397,20 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
 #pragma unroll
       for (int a = 0; a < TR; ++a)
 #pragma unroll
-        for (int b = 0; b < TC; ++b) acc[a][b] = mad_wide(a21[a][q], nm[b], acc[a][b]);
+        for (int b = 0; b < TC; ++b) {
+          const bool fresh = P31 && (q & 1);                   // q = 1, 3, 5, 7 open a new pair
+          acc[a][b] = mad_wide(a21[a][q], nm[b], fresh ? 0ull : acc[a][b]);
+          if (P31 && (q % 2 == 0 || q == GJ_B - 1)) {         // fold after q = 0, 2, 4, 6, 7
+            const uint32_t v = gj_red2(acc[a][b], m);
+            sum[a][b] = q == 0 ? v : add_mod(sum[a][b], v, m.p);
+          }
+        }
     }
 #pragma unroll
     for (int a = 0; a < TR; ++a) {
       uint32_t v[TC];
 #pragma unroll
-      for (int b = 0; b < TC; ++b) v[b] = gj_red(acc[a][b], m);
+      for (int b = 0; b < TC; ++b) v[b] = P31 ? sum[a][b] : gj_red(acc[a][b], m);
       gj_st_sw<TC>(A + (i0 + a) * S + cc, sw, v);
     }
     ti += dti; tc += dtc;
@@ -409,7 +418,7 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
   }
 }
 
-template <int LPM>
+template <int LPM, bool P31>
 __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem, uint32_t cR, int l, const Mod32& m) {
   // largest tile that keeps >= ~70 % of the lanes busy
   auto util = [&](int tr, int tc) {
@@ -418,14 +427,14 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
     return (float)t / (float)(passes * LPM);
   };
   // 2x8 tiles need ~70 registers: only when fewer than 4 CTAs share an SM
-  constexpr int minb = LPM == 8 ? PDB_GJ_MINB8 : PDB_GJ_MINB;
+  constexpr int minb = PDB_GJ_MINB;
 #ifndef PDB_GJ_T28
 #define PDB_GJ_T28 0   // 2x8 trailing tiles: more reuse but spills at 128 registers (measured slower)
 #endif
-  if (PDB_GJ_T28 && minb < 4 && util(2, 8) >= 0.7f) gj_tpass<2, 8, LPM>(A, S, K, mrem, cR, l, m);
-  else if (util(2, 4) >= 0.7f) gj_tpass<2, 4, LPM>(A, S, K, mrem, cR, l, m);
-  else if (util(1, 4) >= 0.7f) gj_tpass<1, 4, LPM>(A, S, K, mrem, cR, l, m);
-  else gj_tpass<1, 2, LPM>(A, S, K, mrem, cR, l, m);
+  if (PDB_GJ_T28 && minb < 4 && util(2, 8) >= 0.7f) gj_tpass<2, 8, LPM, P31>(A, S, K, mrem, cR, l, m);
+  else if (util(2, 4) >= 0.7f) gj_tpass<2, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
+  else if (util(1, 4) >= 0.7f) gj_tpass<1, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
+  else gj_tpass<1, 2, LPM, P31>(A, S, K, mrem, cR, l, m);
 }
 
 // ---- M pass: negM[j][c] = sum_q negX[j][q] A12[q][c], in place in pivot rows K..K+7 ----
@@ -433,7 +442,7 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
 // block of A12 and RPI rows of negX (16 B loads) for RPI*TC*8 MACs.  Items are
 // numbered column-group major, so the lanes sharing a column group work in the
 // same pass; they read it completely before any of them overwrites it.
-template <int RPI, int TC, int LPM>
+template <int RPI, int TC, int LPM, bool P31>
 __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S, int K, int mrem, int l,
                                          unsigned omask, const Mod32& m) {
   constexpr int NRG = GJ_B / RPI;
@@ -456,12 +465,21 @@ __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S,
 #pragma unroll
         for (int t = 0; t < RPI; ++t)
 #pragma unroll
-          for (int b = 0; b < TC; ++b) acc[t][b] = mad_wide(x[t][q], a[b], q ? acc[t][b] : 0ull);
+          for (int b = 0; b < TC; ++b) {
+            const bool fresh = q == 0 || (P31 && q % 2 == 0);
+            acc[t][b] = mad_wide(x[t][q], a[b], fresh ? 0ull : acc[t][b]);
+            if (P31 && (q & 1)) {                              // fold pairs (0,1), (2,3), ...
+              const uint32_t v = gj_red2(acc[t][b], m);
+              res[t][b] = q == 1 ? v : add_mod(res[t][b], v, m.p);
+            }
+          }
       }
+      if (!P31) {
 #pragma unroll
-      for (int t = 0; t < RPI; ++t)
+        for (int t = 0; t < RPI; ++t)
 #pragma unroll
-        for (int b = 0; b < TC; ++b) res[t][b] = gj_red(acc[t][b], m);
+          for (int b = 0; b < TC; ++b) res[t][b] = gj_red(acc[t][b], m);
+      }
     }
     if (NRG > 1) __syncwarp(omask);
     if (act) {
@@ -471,7 +489,7 @@ __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S,
   }
 }
 
-template <int LPM>
+template <int LPM, bool P31>
 __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, int S, int K, int mrem, int l,
                                              unsigned omask, const Mod32& m) {
   auto util = [&](int rpi, int tc) {
@@ -481,17 +499,17 @@ __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, in
 #ifndef PDB_GJ_M44
 #define PDB_GJ_M44 0   // 4x4 M-pass tiles (measured slower than 2x4 at 128 registers)
 #endif
-  if (PDB_GJ_M44 && util(4, 4) >= 0.74f) gj_mpass<4, 4, LPM>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(2, 4) >= 0.74f) gj_mpass<2, 4, LPM>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(4, 2) >= 0.74f) gj_mpass<4, 2, LPM>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(1, 4) >= 0.74f) gj_mpass<1, 4, LPM>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(2, 2) >= 0.74f) gj_mpass<2, 2, LPM>(A, NX, S, K, mrem, l, omask, m);
-  else gj_mpass<1, 2, LPM>(A, NX, S, K, mrem, l, omask, m);
+  if (PDB_GJ_M44 && util(4, 4) >= 0.74f) gj_mpass<4, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(2, 4) >= 0.74f) gj_mpass<2, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(4, 2) >= 0.74f) gj_mpass<4, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(1, 4) >= 0.74f) gj_mpass<1, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(2, 2) >= 0.74f) gj_mpass<2, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  else gj_mpass<1, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
 }
 
 // ---- the kernel ------------------------------------------------------------------------------
-template <class Src, bool DFT8, int LPM>
-__global__ void __launch_bounds__(256, LPM == 8 ? PDB_GJ_MINB8 : PDB_GJ_MINB)
+template <class Src, bool DFT8, int LPM, bool P31>
+__global__ void __launch_bounds__(256, PDB_GJ_MINB)
 det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t nodes,
               uint32_t* __restrict__ num_out, uint32_t* __restrict__ den_out,
               unsigned long long* __restrict__ flag_count, int64_t* __restrict__ flag_nodes, GjGeom g, Mod32 m) {
@@ -580,10 +598,10 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       }
       __syncwarp(omask);
       // ---------------- M: negM = negX * A12, in place in the pivot rows ----------------
-      gj_mpass_any<LPM>(A, NX, S, K, mrem, l, omask, m);
+      gj_mpass_any<LPM, P31>(A, NX, S, K, mrem, l, omask, m);
       __syncwarp(omask);
       // ---------------- T: trailing rows ----------------
-      gj_tpass_any<LPM>(A, S, K, mrem, cR, l, m);
+      gj_tpass_any<LPM, P31>(A, S, K, mrem, cR, l, m);
       __syncwarp(omask);
     }
     if (l == 0) {
@@ -650,16 +668,6 @@ inline GjGeom gj_geom(int r, int warps, int lpm, bool dft8) {
 
 inline size_t gj_smem(const GjGeom& g) {
   return sizeof(uint32_t) * (size_t)g.M * g.MS;
-}
-
-// lanes per matrix (measured on B200, profiles/README_r01.md: 16 beats 32 and 8 at r = 40 and at r = 10..16)
-inline int gj_lpm(int r) {
-  static const char* env = getenv("PDB_GJ_LPM");
-  if (env && *env) {
-    const int v = atoi(env);
-    return v == 8 || v == 16 ? v : 32;
-  }
-  return 16;
 }
 
 // warps per CTA: DFT-8 needs M % 8 == 0; otherwise as many resident matrices as fit
