@@ -24,6 +24,10 @@
 #include "pdb_internal.cuh"
 #include "det_gj.cuh"
 
+#ifndef PDB_GJ_LANES
+#define PDB_GJ_LANES 16   // lanes per matrix (measured best at r = 10..40; 8 and 32 build for experiments)
+#endif
+
 namespace pdb {
 
 struct FlagList {
@@ -251,10 +255,10 @@ template <class Src, bool DFT8>
 static int launch_gj_mode(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int64_t node_lo, int64_t nodes,
                          uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
   // 16 lanes per matrix (the measured best for every order); 2^30 <= p < 2^31 reduces pairs of products
-  const GjGeom g = gj_pick(r, 16, DFT8);
+  const GjGeom g = gj_pick(r, PDB_GJ_LANES, DFT8);
   if (ctx->m.fast())
-    return launch_gj_geom<Src, DFT8, 16, false>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
-  return launch_gj_geom<Src, DFT8, 16, true>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+    return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+  return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, true>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
 }
 
 static int launch_gj(PrimeCtx* ctx, int r, StagedSrc src, const int32_t* ids, int64_t node_lo, int64_t nodes,
@@ -264,7 +268,7 @@ static int launch_gj(PrimeCtx* ctx, int r, StagedSrc src, const int32_t* ids, in
 
 static int launch_gj(PrimeCtx* ctx, int r, FusedSrc src, const int32_t* ids, int64_t node_lo, int64_t nodes,
                      uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
-  const GjGeom g = gj_pick(r, 16, true);
+  const GjGeom g = gj_pick(r, PDB_GJ_LANES, true);
   const bool dft8 = src.E <= 8 && src.NL >= 8 && src.NL % (8 * g.U) == 0 && node_lo % src.NL == 0 &&
                     nodes % src.NL == 0;
   if (dft8) return launch_gj_mode<FusedSrc, true>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
