@@ -37,37 +37,38 @@ class Prediction:
     total_seconds: float
 
 
-def _round_half_up(x: float) -> Decimal:
+def _cents(x: float) -> Decimal:
+    """x rounded half-up to 0.01, from its shortest decimal repr (the reference's rounding)."""
     return Decimal(repr(float(x))).quantize(Decimal("0.01"), rounding=ROUND_HALF_UP)
 
 
 def predicted_total(prime_count: int, order: int, unique_count: int, mean_seconds) -> float:
-    """Total-seconds forecast: primes * order^2 * round(mean, 2) * (k / order^2)."""
-    if order < 1 or not 0 < unique_count <= order * order:
+    """Total-seconds forecast C_p * r^2 * round(T_e, 2) * mu with mu = k / r^2.
+
+    r^2 cancels against mu, so the value is C_p * k * round(T_e, 2), computed in
+    exact decimals before the final float conversion."""
+    if order < 1 or unique_count < 1 or unique_count > order * order:
         raise ValueError(f"unique_count {unique_count} out of range for order {order}")
-    return float(_round_half_up(mean_seconds) * prime_count * unique_count)
+    return float(_cents(mean_seconds) * prime_count * unique_count)
+
+
+def _entry_transform_seconds(m: PolyMatrix, pl: Plan, index: int, table: TwiddleTable) -> float:
+    """Wall seconds of one unique entry's forward transform on the plan grid
+    (reduction and padding are outside the timed call, as in the reference)."""
+    grid = pad_to(reduce_mod(m.unique_entries[index % m.k], table.prime), pl.shape)
+    t0 = time.perf_counter()
+    ntt_forward_multi(grid, table)
+    return time.perf_counter() - t0
 
 
 def predict(m: PolyMatrix, pl: Plan, sample_size: int = 3) -> Prediction:
-    """Time a few unique-entry transforms under one prime and extrapolate."""
+    """Forecast the run time from `sample_size` timed entry transforms under the
+    plan's first prime (entries taken cyclically)."""
     if sample_size < 1:
         raise ValueError("sample_size must be positive")
-    prime = pl.primes[0]
-    table = TwiddleTable(prime)
-    samples = []
-    for i in range(sample_size):
-        entry = m.unique_entries[i % m.k]
-        grid = pad_to(reduce_mod(entry, prime), pl.shape)
-        start = time.perf_counter()
-        ntt_forward_multi(grid, table)
-        samples.append(time.perf_counter() - start)
-    mean = sum(samples) / len(samples)
-    return Prediction(
-        prime_count=pl.prime_count,
-        order=pl.r,
-        unique_count=pl.unique_count,
-        replication=pl.mu,
-        sample_seconds=tuple(samples),
-        mean_rounded=_round_half_up(mean),
-        total_seconds=predicted_total(pl.prime_count, pl.r, pl.unique_count, mean),
-    )
+    table = TwiddleTable(pl.primes[0])
+    times = tuple(_entry_transform_seconds(m, pl, i, table) for i in range(sample_size))
+    mean = sum(times) / sample_size
+    return Prediction(prime_count=pl.prime_count, order=pl.r, unique_count=pl.unique_count,
+                      replication=pl.mu, sample_seconds=times, mean_rounded=_cents(mean),
+                      total_seconds=predicted_total(pl.prime_count, pl.r, pl.unique_count, mean))
