@@ -247,3 +247,32 @@ def test_reference_module_names_resolve():
         m = importlib.import_module("paper_2010_12117_b200." + mod)
         missing = [n for n in names if not hasattr(m, n)]
         assert not missing, (mod, missing)
+
+
+def test_reference_error_messages_before_any_device_work():
+    """The reference's tests match these message substrings (test_determinant.py:188-192,
+    test_crt.py:155-161, test_tensor.py:182-185, test_modular.py:59, 105-107); here they
+    are raised by host-side validation, before any kernel runs."""
+    from paper_2010_12117_b200 import (ModTensor, combine_tensor, det_grid, find_fourier_primes,
+                                       find_root_of_order, inv_mod, poly_matrix)
+    spec = find_fourier_primes(5, 1, start=97, min_count=1)[0]
+    a, b = np.zeros(4, dtype=np.int64), np.zeros(5, dtype=np.int64)
+    with pytest.raises(ValueError, match="share one shape"):
+        det_grid([a, b, a, b], 2, spec)
+    with pytest.raises(ValueError, match="need 4 entry ids"):
+        det_grid([a, a], 2, spec, entry_ids=[0, 1, 1])
+    with pytest.raises(ValueError, match="missing grid"):
+        det_grid([a, a], 2, spec, entry_ids=[0, 1, 2, 0])
+    s1, s2 = find_fourier_primes(3, 2, start=10**9, min_count=2)
+    t1 = ModTensor((2,), np.array([1, 2], dtype=np.int64), s1, ("x",))
+    t2 = ModTensor((4,), np.array([1, 2, 3, 4], dtype=np.int64), s2, ("x",))
+    with pytest.raises(ValueError, match="share one shape"):
+        combine_tensor([t1, t2])
+    with pytest.raises(ValueError, match="at least one residue tensor"):
+        combine_tensor([])
+    with pytest.raises(ValueError, match="square"):
+        poly_matrix([[{}, {}], [{}]], ("x",))
+    with pytest.raises(ValueError, match="no inverse"):
+        inv_mod(0, 97)
+    with pytest.raises(ValueError, match="order unavailable"):
+        find_root_of_order(97, 64)
