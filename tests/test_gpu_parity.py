@@ -444,3 +444,24 @@ def test_many_variables_vs_oracle(cuda, monkeypatch, mode):
                              [(s.p, s.omega, s.q) for s in pl.primes])
     assert list(got.coeffs) == want
     assert got.terms() == naive.symbolic_det(rows, nv)
+
+
+def test_fused_mode_workspace_kill_and_resume(cuda, tmp_path, monkeypatch):
+    """Grids too large for the staged layout checkpoint per prime (p{i}/ifft
+    units only, which is all the reference's executor needs to resume); a
+    run killed after any unit resumes to the same result."""
+    from paper_2010_12117_b200 import resume
+    monkeypatch.setattr(executor, "STAGED_LIMIT", 0)   # force the fused layout even with a workspace
+    m, cfg = workloads.harmonic(3, (5, 7), True)
+    reference = run(m, cfg)
+    units = []
+    run(m, PipelineConfig(progress=units.append), workspace=tmp_path / "full")
+    pl = plan(m, cfg)
+    assert units == ["p%d/ifft" % i for i in range(pl.prime_count)] + ["crt"]
+    for cut in range(1, len(units)):
+        ws = tmp_path / ("ws%d" % cut)
+        with pytest.raises(_Abort):
+            run(m, PipelineConfig(progress=_abort_after(cut)), workspace=ws)
+        seen = []
+        assert resume(ws, PipelineConfig(progress=seen.append)).coeffs == reference.coeffs
+        assert seen == units[cut:]
