@@ -465,3 +465,27 @@ def test_fused_mode_workspace_kill_and_resume(cuda, tmp_path, monkeypatch):
         seen = []
         assert resume(ws, PipelineConfig(progress=seen.append)).coeffs == reference.coeffs
         assert seen == units[cut:]
+
+
+def test_resume_reference_written_partial_workspace(cuda, tmp_path):
+    """Cross-resume: a workspace the reference itself wrote and was killed in
+    (tests/golden/make_partial_ws.py, after 7 of 17 units) is finished by this
+    package, which computes exactly the remaining units and returns the
+    reference's result."""
+    import json
+    import shutil
+    from pathlib import Path
+    from paper_2010_12117_b200 import resume
+    here = Path(__file__).resolve().parent / "golden"
+    meta = json.loads((here / "ref_partial_ws.json").read_text())
+    ws = tmp_path / "ws"
+    shutil.copytree(here / "ref_partial_ws", ws)
+    seen = []
+    got = resume(ws, PipelineConfig(progress=seen.append))
+    assert seen == meta["remaining_units"]
+    assert list(got.shape) == meta["shape"]
+    assert got.terms() == {tuple(e): c for e, c in meta["terms"]}
+    # the completed workspace reloads without recomputation
+    again = []
+    assert resume(ws, PipelineConfig(progress=again.append)).coeffs == got.coeffs
+    assert again == []
