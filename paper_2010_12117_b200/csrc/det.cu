@@ -225,23 +225,23 @@ static uint32_t mont_scale(const Mod32& m, int r) {
   return (uint32_t)acc;
 }
 
-template <class Src, bool DFT8, int LPM, bool P31>
+template <class Src, bool DFT8, int LPM, bool P31, int RPC>
 static int launch_gj_geom(PrimeCtx* ctx, const GjGeom& g, Src src, const int32_t* ids, int64_t node_lo,
                           int64_t nodes, uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn,
                           cudaStream_t st) {
   const size_t smem = gj_smem(g);
-  if (cudaFuncSetAttribute(det_gj_kernel<Src, DFT8, LPM, P31>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(det_gj_kernel<Src, DFT8, LPM, P31, RPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return check_launch("det_gj attribute");
   int ctas_per_sm = 0;
   const int threads = g.M * LPM;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, det_gj_kernel<Src, DFT8, LPM, P31>, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, det_gj_kernel<Src, DFT8, LPM, P31, RPC>, threads, smem);
   if (ctas_per_sm < 1) ctas_per_sm = 1;
   const int64_t iters = DFT8 ? nodes / g.M : (nodes + g.M - 1) / g.M;
   const int64_t cap = (int64_t)ctx->sms * ctas_per_sm;
   const int grid = (int)(iters < cap ? iters : cap);
   if (grid < 1) return 0;
-  det_gj_kernel<Src, DFT8, LPM, P31><<<grid, threads, smem, st>>>(src, ids, node_lo, nodes, out, den, fc, fn, g, ctx->m);
+  det_gj_kernel<Src, DFT8, LPM, P31, RPC><<<grid, threads, smem, st>>>(src, ids, node_lo, nodes, out, den, fc, fn, g, ctx->m);
   count_launch();
   if (int rc = check_launch("det_gj")) return rc;
   const int64_t fblocks = (nodes + 255) / 256;
@@ -256,9 +256,15 @@ static int launch_gj_mode(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int
                          uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
   // 16 lanes per matrix (the measured best for every order); 2^30 <= p < 2^31 reduces pairs of products
   const GjGeom g = gj_pick(r, PDB_GJ_LANES, DFT8);
-  if (ctx->m.fast())
-    return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
-  return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, true>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+  if (ctx->m.fast()) {
+    // compile-time orders for the common sizes (C5: 40, C3: 16)
+    if (g.RP == 40 && !getenv("PDB_GJ_NO_RPC"))
+      return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 40>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+    if (g.RP == 16 && !getenv("PDB_GJ_NO_RPC"))
+      return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 16>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+    return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 0>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+  }
+  return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, true, 0>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
 }
 
 static int launch_gj(PrimeCtx* ctx, int r, StagedSrc src, const int32_t* ids, int64_t node_lo, int64_t nodes,

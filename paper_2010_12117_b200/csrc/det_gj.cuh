@@ -421,19 +421,20 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
 template <int LPM, bool P31>
 __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem, uint32_t cR, int l, const Mod32& m) {
   // largest tile that keeps >= ~70 % of the lanes busy
-  auto util = [&](int tr, int tc) {
+  // fraction of lane slots busy >= pct/100, in integers
+  auto util = [&](int tr, int tc, int pct) {
     const int t = (mrem / tr) * (mrem / tc);
     const int passes = (t + LPM - 1) / LPM;
-    return (float)t / (float)(passes * LPM);
+    return 100 * t >= pct * passes * LPM;
   };
   // 2x8 tiles need ~70 registers: only when fewer than 4 CTAs share an SM
   constexpr int minb = PDB_GJ_MINB;
 #ifndef PDB_GJ_T28
 #define PDB_GJ_T28 0   // 2x8 trailing tiles: more reuse but spills at 128 registers (measured slower)
 #endif
-  if (PDB_GJ_T28 && minb < 4 && util(2, 8) >= 0.7f) gj_tpass<2, 8, LPM, P31>(A, S, K, mrem, cR, l, m);
-  else if (util(2, 4) >= 0.7f) gj_tpass<2, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
-  else if (util(1, 4) >= 0.7f) gj_tpass<1, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
+  if (PDB_GJ_T28 && minb < 4 && util(2, 8, 70)) gj_tpass<2, 8, LPM, P31>(A, S, K, mrem, cR, l, m);
+  else if (util(2, 4, 70)) gj_tpass<2, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
+  else if (util(1, 4, 70)) gj_tpass<1, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
   else gj_tpass<1, 2, LPM, P31>(A, S, K, mrem, cR, l, m);
 }
 
@@ -492,32 +493,41 @@ __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S,
 template <int LPM, bool P31>
 __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, int S, int K, int mrem, int l,
                                              unsigned omask, const Mod32& m) {
-  auto util = [&](int rpi, int tc) {
+  auto util = [&](int rpi, int tc, int pct) {
     const int t = (mrem / tc) * (GJ_B / rpi);
-    return (float)t / (float)(((t + LPM - 1) / LPM) * LPM);
+    return 100 * t >= pct * ((t + LPM - 1) / LPM) * LPM;
   };
 #ifndef PDB_GJ_M44
 #define PDB_GJ_M44 0   // 4x4 M-pass tiles (measured slower than 2x4 at 128 registers)
 #endif
-  if (PDB_GJ_M44 && util(4, 4) >= 0.74f) gj_mpass<4, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(2, 4) >= 0.74f) gj_mpass<2, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(4, 2) >= 0.74f) gj_mpass<4, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(1, 4) >= 0.74f) gj_mpass<1, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(2, 2) >= 0.74f) gj_mpass<2, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  if (PDB_GJ_M44 && util(4, 4, 74)) gj_mpass<4, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(2, 4, 74)) gj_mpass<2, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(4, 2, 74)) gj_mpass<4, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(1, 4, 74)) gj_mpass<1, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(2, 2, 74)) gj_mpass<2, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
   else gj_mpass<1, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
 }
 
 // ---- the kernel ------------------------------------------------------------------------------
-template <class Src, bool DFT8, int LPM, bool P31>
+#ifndef PDB_GJ_ABL
+#define PDB_GJ_ABL 0   // profiling ablation only (1: no M pass, 2: no T pass, 3: one fill per CTA); results are wrong
+#endif
+// RPC > 0: the padded order is the compile-time constant RPC (row stride
+// gj_row_stride(RPC)); the block loop unrolls, every pass sees a constant
+// trailing size, and all shared-memory addressing folds into immediates.
+template <class Src, bool DFT8, int LPM, bool P31, int RPC>
 __global__ void __launch_bounds__(256, PDB_GJ_MINB)
 det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t nodes,
               uint32_t* __restrict__ num_out, uint32_t* __restrict__ den_out,
               unsigned long long* __restrict__ flag_count, int64_t* __restrict__ flag_nodes, GjGeom g, Mod32 m) {
   static_assert(LPM == 8 || LPM == 16 || LPM == 32, "8, 16 or 32 lanes per matrix");
+  static_assert(RPC % GJ_B == 0, "compile-time order must be padded to the block size");
   constexpr int LPR = LPM / 8;   // lanes per pivot-block row
   constexpr int EPL = 8 / LPR;   // pivot-block elements per lane
   extern __shared__ __align__(16) uint32_t smem[];
-  const int r = g.r, RP = g.RP, S = g.S;
+  const int r = g.r;
+  const int RP = RPC ? RPC : g.RP;
+  const int S = RPC ? gj_row_stride(RPC) : g.S;
   const int32_t* ids = ids_g;     // read through L1 by the fills
   uint32_t* mats = smem;
   const int lane = threadIdx.x & 31;
@@ -539,7 +549,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
 
   for (int64_t it = blockIdx.x; it < iters; it += gridDim.x) {
     __syncthreads();
-    if constexpr (DFT8) gj_fill_dft8(src, mats, g, ids, it, node_lo, one, dense);
+    if constexpr (DFT8) { if (PDB_GJ_ABL != 3 || it == blockIdx.x) gj_fill_dft8(src, mats, g, ids, it, node_lo, one, dense); }
     else gj_fill(src, mats, g, ids, it, node_lo, nodes, one, dense);
     __syncthreads();
     int64_t node;
@@ -549,6 +559,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
 
     uint32_t num = one, den = one, Q = one, C = one;
     bool ok = true;
+#pragma unroll
     for (int K = 0; K < RP; K += GJ_B) {
       const int mrem = RP - K - GJ_B;
       // ---------------- P: Gauss-Jordan on the pivot block ----------------
@@ -598,10 +609,10 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       }
       __syncwarp(omask);
       // ---------------- M: negM = negX * A12, in place in the pivot rows ----------------
-      gj_mpass_any<LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+      if (PDB_GJ_ABL != 1) gj_mpass_any<LPM, P31>(A, NX, S, K, mrem, l, omask, m);
       __syncwarp(omask);
       // ---------------- T: trailing rows ----------------
-      gj_tpass_any<LPM, P31>(A, S, K, mrem, cR, l, m);
+      if (PDB_GJ_ABL != 2) gj_tpass_any<LPM, P31>(A, S, K, mrem, cR, l, m);
       __syncwarp(omask);
     }
     if (l == 0) {

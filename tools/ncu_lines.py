@@ -44,11 +44,16 @@ def line_map(obj, want):
         if m:
             loc = (Path(m.group(1)).name, int(m.group(2)))
             continue
-        m = re.search(r"/\*([0-9a-f]{4,})\*/", ln)
+        m = re.search(r"/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
         if m and cur is not None and loc:
-            cur[int(m.group(1), 16)] = loc
+            cur[int(m.group(1), 16)] = loc + (_opcode(m.group(2)),)
     cands = [f for f in funcs if all(w in f for w in want)]
     return funcs, cands
+
+
+def _opcode(text):
+    w = text.split()
+    return (w[1] if w and w[0].startswith("@") and len(w) > 1 else (w[0] if w else "")).split(".")[0]
 
 
 def num(x):
@@ -71,13 +76,17 @@ def main():
     fn = min(cands, key=lambda f: abs(len(funcs[f]) - n))
     lmap = funcs[fn]
     base = int(rows[0]["Address"], 16)
+    # the object must be the build that was profiled: compare opcodes address by address
+    same = sum(1 for r in rows if lmap.get(int(r["Address"], 16) - base, ("", 0, ""))[2] == _opcode(r["Source"]))
+    if same < 0.95 * len(rows):
+        sys.exit("object does not match the profiled build (%d of %d opcodes agree)" % (same, len(rows)))
     agg = collections.defaultdict(lambda: [0.0, 0.0, 0.0])
     tot = [0.0, 0.0, 0.0]
     reasons = [c for c in rows[0] if c.startswith("stall_") and "Not Issued" not in c]
     why = collections.defaultdict(collections.Counter)
     for r in rows:
         off = int(r["Address"], 16) - base
-        loc = lmap.get(off, ("?", 0))
+        loc = lmap.get(off, ("?", 0, ""))[:2]
         v = (num(r["Thread Instructions Executed"]), num(r["Warp Stall Sampling (All Samples)"]),
              num(r["Instructions Executed"]))
         for i in range(3):
