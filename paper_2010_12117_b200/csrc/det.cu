@@ -258,9 +258,11 @@ static int launch_gj_mode(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int
   const GjGeom g = gj_pick(r, PDB_GJ_LANES, DFT8);
   if (ctx->m.fast()) {
     // compile-time orders for the common sizes (C5: 40, C3: 16)
-    if (g.RP == 40 && !getenv("PDB_GJ_NO_RPC"))
+    // (the compile-time kernels assume 256-thread CTAs)
+    const bool rpc = g.M * PDB_GJ_LANES == 256 && !getenv("PDB_GJ_NO_RPC");
+    if (g.RP == 40 && rpc)
       return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 40>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
-    if (g.RP == 16 && !getenv("PDB_GJ_NO_RPC"))
+    if (g.RP == 16 && rpc)
       return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 16>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
     return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 0>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
   }

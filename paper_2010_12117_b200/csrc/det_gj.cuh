@@ -46,6 +46,13 @@ constexpr int GJ_B = 8;
 __host__ __device__ constexpr int gj_nx_row(int j) { return j * GJ_B + (j / 4) * 4; }
 constexpr int GJ_NX_WORDS = 8 * GJ_B + 4;
 
+// matrix stride (words) for padded order RP: RP rows + negX, padded to 16 mod 32
+// (the two matrices of a warp, and the U matrices a fill group writes, start in
+// opposite bank halves)
+__host__ __device__ constexpr int gj_matrix_stride(int RP, int S) {
+  return RP * S + GJ_NX_WORDS + ((16 - (RP * S + GJ_NX_WORDS) % 32) + 32) % 32;
+}
+
 #ifndef PDB_GJ_MINB
 #define PDB_GJ_MINB 2   // resident 256-thread CTAs per SM the register budget is sized for
 #endif
@@ -63,7 +70,7 @@ struct GjGeom {
 #define PDB_GJ_ROWPAD 0   // extra words per matrix row (0: densest packing, most resident matrices)
 #endif
 
-__host__ __device__ inline int gj_row_stride(int RP) { return RP + PDB_GJ_ROWPAD; }
+__host__ __device__ constexpr int gj_row_stride(int RP) { return RP + PDB_GJ_ROWPAD; }
 
 // REDC of a <= 9-product accumulator, canonical: two conditional subtractions.
 __device__ __forceinline__ uint32_t gj_red(uint64_t acc, const Mod32& m) {
@@ -227,10 +234,13 @@ __device__ __forceinline__ void gj_fill_dft8_e(const FusedSrc& src, uint32_t* ma
 // Dense case (entry_ids[p] == p, no padding: the C3/C5 shape): position p is
 // entry p and smem word p of its matrix, so addressing is affine and four
 // positions (4E coalesced loads) are kept in flight per thread.
-template <int E>
+// UC, MSC, NC > 0: compile-time U, matrix stride and r^2 (256-thread CTAs), so
+// the shared-memory stores and the coefficient loads use immediate offsets.
+template <int E, int UC = 0, int MSC = 0, int NC = 0>
 __device__ __forceinline__ void gj_fill_dft8_dense(const FusedSrc& src, uint32_t* mats, const GjGeom& g,
                                                    int64_t it, int64_t node_lo) {
-  const int U = g.U, NL = src.NL, k = src.k, n = g.r * g.r;
+  const int U = UC ? UC : g.U, NL = src.NL, k = src.k, n = NC ? NC : g.r * g.r;
+  const int MS = MSC ? MSC : g.MS;
   const uint32_t p = src.p;
   const int per_o = NL / (8 * U);
   const int lpo = __ffs(per_o) - 1;   // per_o and NL are powers of two on this path
@@ -254,47 +264,62 @@ __device__ __forceinline__ void gj_fill_dft8_dense(const FusedSrc& src, uint32_t
       if (kk >= NL) kk -= NL;
     }
   }
-  const int ms = U * g.MS;
-  uint32_t* base = mats + uu * g.MS;
+  const int ms = U * MS;
+  uint32_t* base = mats + uu * MS;
   const uint32_t* slab = src.part + o * (int64_t)E * k;
-  const int step = blockDim.x / U;
+  const int step = UC ? 256 / UC : blockDim.x / U;
 #ifndef PDB_GJ_FILLF
 #define PDB_GJ_FILLF 4
 #endif
   constexpr int F = PDB_GJ_FILLF;   // positions in flight
-  for (int p0 = threadIdx.x / U; p0 < n; p0 += F * step) {
+  int p0 = threadIdx.x / U;
+  // one pointer per coefficient row, advanced by a constant: F*E loads per
+  // round from E registers with immediate offsets when the geometry is static
+  const uint32_t* sp[E];
+#pragma unroll
+  for (int l = 0; l < E; ++l) sp[l] = slab + (int64_t)l * k + p0;
+  for (; p0 + (F - 1) * step < n; p0 += F * step) {
     uint32_t c[F][E];
 #pragma unroll
+    for (int f = 0; f < F; ++f)
+#pragma unroll
+      for (int l = 0; l < E; ++l) c[f][l] = __ldg(sp[l] + f * step);
+#pragma unroll
+    for (int l = 0; l < E; ++l) sp[l] += F * step;
+#pragma unroll
     for (int f = 0; f < F; ++f) {
-      const int q = p0 + f * step < n ? p0 + f * step : p0;
+      uint32_t x[8];
+      gj_dft8<E>(c[f], tw, tws, w, ws, p, x);
+      uint32_t* d = base + p0 + f * step;
 #pragma unroll
-      for (int l = 0; l < E; ++l) c[f][l] = __ldg(slab + l * k + q);
+      for (int v = 0; v < 8; ++v) d[v * ms] = x[v];
     }
+  }
+  for (; p0 < n; p0 += step) {   // tail: single positions
+    uint32_t c[E];
 #pragma unroll
-    for (int f = 0; f < F; ++f) {
-      const int q = p0 + f * step;
-      if (q < n) {
-        uint32_t x[8];
-        gj_dft8<E>(c[f], tw, tws, w, ws, p, x);
+    for (int l = 0; l < E; ++l) { c[l] = __ldg(sp[l]); sp[l] += step; }
+    uint32_t x[8];
+    gj_dft8<E>(c, tw, tws, w, ws, p, x);
 #pragma unroll
-        for (int v = 0; v < 8; ++v) base[v * ms + q] = x[v];
-      }
-    }
+    for (int v = 0; v < 8; ++v) base[v * ms + p0] = x[v];
   }
 }
 
+// UC/MSC/NC: compile-time dense-fill geometry (0 = from g), see gj_fill_dft8_dense
+template <int UC = 0, int MSC = 0, int NC = 0>
 __device__ __forceinline__ void gj_fill_dft8(const FusedSrc& src, uint32_t* mats, const GjGeom& g, const int32_t* ids,
                                              int64_t it, int64_t node_lo, uint32_t one, bool dense) {
   if (dense) {
     switch (src.E) {
-      case 1: gj_fill_dft8_dense<1>(src, mats, g, it, node_lo); return;
-      case 2: gj_fill_dft8_dense<2>(src, mats, g, it, node_lo); return;
-      case 3: gj_fill_dft8_dense<3>(src, mats, g, it, node_lo); return;
-      case 4: gj_fill_dft8_dense<4>(src, mats, g, it, node_lo); return;
-      case 5: gj_fill_dft8_dense<5>(src, mats, g, it, node_lo); return;
-      case 6: gj_fill_dft8_dense<6>(src, mats, g, it, node_lo); return;
-      case 7: gj_fill_dft8_dense<7>(src, mats, g, it, node_lo); return;
-      default: gj_fill_dft8_dense<8>(src, mats, g, it, node_lo); return;
+      case 1: gj_fill_dft8_dense<1, UC, MSC, NC>(src, mats, g, it, node_lo); return;
+      case 2: gj_fill_dft8_dense<2, UC, MSC, NC>(src, mats, g, it, node_lo); return;
+      case 3: gj_fill_dft8_dense<3, UC, MSC, NC>(src, mats, g, it, node_lo); return;
+      case 4: gj_fill_dft8_dense<4, UC, MSC, NC>(src, mats, g, it, node_lo); return;
+      case 5: gj_fill_dft8_dense<5, UC, MSC, NC>(src, mats, g, it, node_lo); return;
+      case 6: gj_fill_dft8_dense<6, UC, MSC, NC>(src, mats, g, it, node_lo); return;
+      case 7: gj_fill_dft8_dense<7, UC, MSC, NC>(src, mats, g, it, node_lo); return;
+      default: gj_fill_dft8_dense<8, UC, MSC, NC>(src, mats, g, it, node_lo); return;
     }
   }
   switch (src.E) {
@@ -530,11 +555,12 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
   const int S = RPC ? gj_row_stride(RPC) : g.S;
   const int32_t* ids = ids_g;     // read through L1 by the fills
   uint32_t* mats = smem;
+  const int MS = RPC ? gj_matrix_stride(RPC, gj_row_stride(RPC)) : g.MS;
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPM, l = lane % LPM;
   const unsigned omask = (LPM == 32 ? 0xffffffffu : ((1u << LPM) - 1u)) << (grp * LPM);
   const int slot = (threadIdx.x >> 5) * (32 / LPM) + grp;
-  uint32_t* A = mats + (size_t)slot * g.MS;
+  uint32_t* A = mats + (size_t)slot * MS;
   uint32_t* NX = A + RP * S;          // negX [8][8]
   const uint32_t p = m.p, one = m.r1;
   const int pj = l / LPR, pc = EPL * (l % LPR);   // my pivot-block row / first column
@@ -549,7 +575,15 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
 
   for (int64_t it = blockIdx.x; it < iters; it += gridDim.x) {
     __syncthreads();
-    if constexpr (DFT8) { if (PDB_GJ_ABL != 3 || it == blockIdx.x) gj_fill_dft8(src, mats, g, ids, it, node_lo, one, dense); }
+    if constexpr (DFT8) {
+      if (PDB_GJ_ABL != 3 || it == blockIdx.x) {
+        if constexpr (RPC > 0)   // launched with 256 threads, M = 256 / LPM matrices, RP = RPC
+          gj_fill_dft8<256 / LPM / 8, gj_matrix_stride(RPC, gj_row_stride(RPC)), RPC * RPC>(src, mats, g, ids, it,
+                                                                                           node_lo, one, dense);
+        else
+          gj_fill_dft8(src, mats, g, ids, it, node_lo, one, dense);
+      }
+    }
     else gj_fill(src, mats, g, ids, it, node_lo, nodes, one, dense);
     __syncthreads();
     int64_t node;
@@ -577,13 +611,21 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         uint32_t prow[EPL];
 #pragma unroll
         for (int k = 0; k < EPL; ++k) prow[k] = __shfl_sync(omask, v[k], s * LPR + l % LPR, LPM);
-        zl = pj == s ? lam : zl;
-        const uint32_t nt = p - t;   // in (0, p]: a valid multiplier for the 2-product REDC
+        // Row s keeps its values (its prow is itself: 0 * v + 1 * v) and takes lam
+        // at column s; other rows: z v - t prow, with -t lam at column s.
+        const bool piv = pj == s;
+        zl = piv ? lam : zl;
+        const uint32_t zz = piv ? 0u : z;
+        const uint32_t nn = piv ? one : p - t;   // p - t in (0, p]: a valid 2-product multiplier
 #pragma unroll
         for (int k = 0; k < EPL; ++k) {
-          const bool diag = pc + k == s;
-          const uint32_t nv = gj_red2(mad_wide(z, diag ? 0u : v[k], mad_wide(nt, diag ? lam : prow[k], 0ull)), m);
-          v[k] = pj != s ? nv : (diag ? lam : v[k]);
+          uint32_t a = v[k], b = prow[k];
+          if (k == s % EPL) {   // the only element of this lane that can sit in column s
+            const bool diag = pc == s - s % EPL;
+            a = diag ? 0u : a;
+            b = diag ? lam : b;
+          }
+          v[k] = gj_red2(mad_wide(zz, a, mad_wide(nn, b, 0ull)), m);
         }
         if (s == GJ_B - 1) z7 = z;
         lam = gj_mont(lam, z, m);
@@ -670,8 +712,7 @@ inline GjGeom gj_geom(int r, int warps, int lpm, bool dft8) {
   g.S = gj_row_stride(g.RP);
   // matrix stride = 16 (mod 32) words: the two matrices of a warp (and the U
   // matrices a fill thread group writes) start in opposite bank halves
-  g.MS = g.RP * g.S + GJ_NX_WORDS;
-  g.MS += ((16 - g.MS % 32) + 32) % 32;
+  g.MS = gj_matrix_stride(g.RP, g.S);
   g.M = warps * (32 / lpm);
   g.U = dft8 ? g.M / 8 : 0;
   return g;

@@ -227,6 +227,8 @@ def test_modes_agree_on_harmonic_rung(cuda, mode, monkeypatch):
     (9, 2, (3, 4), 2),     # padded order (RP = 16), DFT-8 fill, non-dense positions
     (10, 3, (1, 1, 6), 3), # 3 variables, E = 7
     (10, 2, (1, 2), 4),    # short last axis (N = 32): U-group divisibility edge
+    (16, 2, (1, 2), 6),    # compile-time order 16, dense DFT-8 fill
+    (34, 1, (1,), 5),      # compile-time order 40 with 6 padded rows, one variable
 ])
 def test_fused_mode_edge_shapes_vs_oracle(cuda, monkeypatch, r, vn, degs, seed):
     """The fused path (partial forward NTT + in-kernel last-axis evaluation) at
