@@ -377,6 +377,7 @@ def run_ours(args):
         traffic_note = ("dram read+write bytes per launch of %d nodes, scaled from %s (%d-node launch)"
                         % (launch_nodes, t["source"], t["nodes_per_launch"]))
         ncu_summary = {k: t[k] for k in ("pipes_pct_of_peak", "issue_active_pct", "warp_instructions_per_det",
+                                          "issue_model_cycles_per_det", "issue_model_cycles_frac",
                                           "dram_bytes_per_node", "source") if k in t}
     out = {
         "metric": "mod-p %dx%d dets/sec (%s)" % (r, r, args.config.upper()),
