@@ -457,7 +457,11 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
 #ifndef PDB_GJ_T28
 #define PDB_GJ_T28 0   // 2x8 trailing tiles: more reuse but spills at 128 registers (measured slower)
 #endif
+#ifndef PDB_GJ_T44
+#define PDB_GJ_T44 0   // 4x4 trailing tiles (experiment)
+#endif
   if (PDB_GJ_T28 && minb < 4 && util(2, 8, 70)) gj_tpass<2, 8, LPM, P31>(A, S, K, mrem, cR, l, m);
+  else if (PDB_GJ_T44 && util(4, 4, 70)) gj_tpass<4, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
   else if (util(2, 4, 70)) gj_tpass<2, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
   else if (util(1, 4, 70)) gj_tpass<1, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
   else gj_tpass<1, 2, LPM, P31>(A, S, K, mrem, cR, l, m);
