@@ -15,6 +15,42 @@
 #include <cstdint>
 #include <cstring>
 
+// CPython 3.12/3.13 store an int as 30-bit digits behind a tag word
+// (digit count << 3 | sign: 0 positive, 2 negative).  Building the object
+// directly from the limb bit stream skips _PyLong_FromByteArray's byte loop
+// and, for negative values, the second allocation of PyNumber_Negative.
+#if PY_VERSION_HEX >= 0x030C0000 && PY_VERSION_HEX < 0x030E0000 && PYLONG_BITS_IN_DIGIT == 30
+#define PDB_DIRECT_LONG 1
+static PyObject* long_from_limbs(const unsigned char* row, Py_ssize_t width, bool negative) {
+  digit buf[80];   // up to 74 limbs = 2368 bits
+  Py_ssize_t nd = 0;
+  uint64_t acc = 0;
+  int bits = 0;
+  for (Py_ssize_t w = 0; w < width; ++w) {
+    uint32_t limb;
+    std::memcpy(&limb, row + 4 * w, 4);
+    acc |= (uint64_t)limb << bits;
+    bits += 32;
+    while (bits >= PyLong_SHIFT) {
+      buf[nd++] = (digit)(acc & PyLong_MASK);
+      acc >>= PyLong_SHIFT;
+      bits -= PyLong_SHIFT;
+    }
+  }
+  if (bits > 0) buf[nd++] = (digit)acc;
+  while (nd > 0 && buf[nd - 1] == 0) --nd;
+  if (nd <= 2) {   // fits in 60 bits: the public constructor (keeps small ints canonical)
+    long long v = nd == 0 ? 0 : (long long)buf[0] | (nd == 2 ? (long long)buf[1] << PyLong_SHIFT : 0);
+    return PyLong_FromLongLong(negative ? -v : v);
+  }
+  PyLongObject* op = _PyLong_New(nd);
+  if (!op) return nullptr;
+  std::memcpy(op->long_value.ob_digit, buf, (size_t)nd * sizeof(digit));
+  if (negative) op->long_value.lv_tag = ((uintptr_t)nd << _PyLong_NON_SIZE_BITS) | 2;
+  return (PyObject*)op;
+}
+#endif
+
 static PyObject* ints_from_limbs(PyObject*, PyObject* args) {
   Py_buffer limbs, index, neg;
   Py_ssize_t n, width;
@@ -46,6 +82,16 @@ static PyObject* ints_from_limbs(PyObject*, PyObject* args) {
       }
       const unsigned char* row = lb + (size_t)j * (size_t)width * 4;
       PyObject* v;
+#ifdef PDB_DIRECT_LONG
+      if (width <= 74) {
+        v = long_from_limbs(row, width, ng[j] != 0);
+        if (!v) { Py_CLEAR(out); goto done; }
+        PyObject* old = PyList_GET_ITEM(out, pos);
+        PyList_SET_ITEM(out, pos, v);
+        Py_DECREF(old);
+        continue;
+      }
+#endif
       if (width <= 2) {
         uint64_t mag = 0;
         std::memcpy(&mag, row, (size_t)width * 4);

@@ -130,33 +130,80 @@ class DevicePlan:
         self.wide = wide_primes([s.p for s in pl.primes])
         self.word = native.word_dtype(self.wide)
         self.staged = staged or self.vn == 0 or self.wide
-        entries, coeffs = [], []
-        for e, t in enumerate(m.unique_entries):
-            for exps, c in t._nonzero():
-                entries.append((e, exps))
-                coeffs.append(c)
-        mag, neg, L = _limbs_of(coeffs)
-        self.count = len(coeffs)
-        self.L = L
-        if self.staged:
-            pos = [e * self.nodes + _flat(exps, self.shape) for e, exps in entries]
-        else:
+        if not self.staged:
             self.E = max(t.shape[-1] for t in m.unique_entries)
             self.outer = self.nodes // self.shape[-1]
-            # [outer][E][k]: entries innermost (coalesced fills in the det kernel)
-            pos = [(_flat(exps[:-1], self.shape[:-1]) * self.E + exps[-1]) * self.k + e
-                   for e, exps in entries]
+        prep = _vector_terms(m, self.shape, self.nodes, self.staged, self.E if not self.staged else 0)
+        if prep is None:
+            prep = _python_terms(m, self.shape, self.nodes, self.staged, self.E if not self.staged else 0)
+        mag, neg, L, pos = prep
+        self.count = len(neg)
+        self.L = L
         self.mag = torch.from_numpy(mag.view(np.int32).copy()).to(device) if self.count else \
             torch.zeros(1, dtype=torch.int32, device=device)
         self.neg = torch.from_numpy(neg.copy()).to(device) if self.count else \
             torch.zeros(1, dtype=torch.uint8, device=device)
-        self.pos = torch.tensor(pos if pos else [0], dtype=torch.int64, device=device)
+        self.pos = torch.from_numpy(np.ascontiguousarray(pos, dtype=np.int64)).to(device) if self.count else \
+            torch.zeros(1, dtype=torch.int64, device=device)
         self.ids = torch.tensor(list(m.entry_ids), dtype=torch.int32, device=device)
         # per-axis coefficient extents (for NTT pruning): largest exponent + 1
         self.ext = [max(t.shape[a] for t in m.unique_entries) for a in range(self.vn)]
 
     def buffer_words(self) -> int:
         return self.k * self.nodes if self.staged else self.k * self.outer * self.E
+
+
+def _python_terms(m: PolyMatrix, shape, nodes, staged, E):
+    """(limbs, negative flags, L, scatter positions) of every nonzero coefficient:
+    staged layout e*nodes + flat(exps); fused layout [outer][E][k] (entries
+    innermost, coalesced fills in the det kernel)."""
+    entries, coeffs = [], []
+    for e, t in enumerate(m.unique_entries):
+        for exps, c in t._nonzero():
+            entries.append((e, exps))
+            coeffs.append(c)
+    mag, neg, L = _limbs_of(coeffs)
+    if staged:
+        pos = [e * nodes + _flat(exps, shape) for e, exps in entries]
+    else:
+        pos = [(_flat(exps[:-1], shape[:-1]) * E + exps[-1]) * m.k + e for e, exps in entries]
+    return mag, neg, L, np.array(pos, dtype=np.int64).reshape(-1)
+
+
+def _vector_terms(m: PolyMatrix, shape, nodes, staged, E):
+    """_python_terms in numpy, same order, when every unique entry has the same
+    coefficient box and all coefficients fit in int64 (None otherwise)."""
+    shapes = {tuple(t.shape) for t in m.unique_entries}
+    if len(shapes) != 1 or not shape:
+        return None
+    box = shapes.pop()
+    if len(box) != len(shape):
+        return None
+    try:
+        C = np.array([t.coeffs for t in m.unique_entries], dtype=np.int64).reshape(m.k, -1)
+    except (OverflowError, ValueError, TypeError):
+        return None
+    e_idx, off = np.nonzero(C)            # entry-major, then row-major offset: the _nonzero order
+    vals = C[e_idx, off]
+    if vals.size and vals.min() == np.iinfo(np.int64).min:
+        return None
+    neg = (vals < 0).astype(np.uint8)
+    mag = np.abs(vals).astype(np.uint64)
+    top = int(mag.max()) if mag.size else 0
+    L = max(1, (top.bit_length() + 31) // 32)
+    limbs = np.stack([(mag & 0xFFFFFFFF).astype(np.uint32), (mag >> np.uint64(32)).astype(np.uint32)], axis=1)[:, :L]
+    exps = np.unravel_index(off, box)
+    if staged:
+        flat = np.zeros(off.shape, dtype=np.int64)
+        for a, n in enumerate(shape):
+            flat = flat * n + exps[a]
+        pos = e_idx.astype(np.int64) * nodes + flat
+    else:
+        flat = np.zeros(off.shape, dtype=np.int64)
+        for a, n in enumerate(shape[:-1]):
+            flat = flat * n + exps[a]
+        pos = (flat * E + exps[-1]) * m.k + e_idx
+    return np.ascontiguousarray(limbs, dtype=np.uint32), neg, L, pos.astype(np.int64)
 
 
 def _flat(exps, shape):

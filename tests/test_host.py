@@ -196,7 +196,7 @@ def test_native_ints_from_limbs_matches_python_path():
     h = native.host_module()
     rng = np.random.default_rng(7)
     n = 5000
-    for L in (1, 2, 3, 9):
+    for L in (1, 2, 3, 9, 74, 75):   # <= 74 limbs: direct digit fill; wider: from_bytes fallback
         limbs = np.zeros((n, L), dtype=np.uint32)
         nz = np.sort(rng.choice(n, 1700, replace=False))
         for i in nz:
@@ -208,6 +208,9 @@ def test_native_ints_from_limbs_matches_python_path():
         keep = np.flatnonzero(limbs.any(axis=1))
         got = h.ints_from_limbs(limbs[keep].tobytes(), keep.astype(np.int64).tobytes(), neg[keep].tobytes(), n, L)
         assert got == want
+        assert all(type(v) is int for v in got)
+        zero = 0
+        assert all(v is zero for v in got if v == 0)   # small ints stay the shared singletons
     with pytest.raises(ValueError):
         h.ints_from_limbs(b"\0" * 8, np.zeros(1, np.int64).tobytes(), b"\0", 4, 1)
     with pytest.raises(IndexError):
