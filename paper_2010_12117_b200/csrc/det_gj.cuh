@@ -8,7 +8,9 @@
 //   with an identity block, which leaves the determinant unchanged):
 //     P  division-free Gauss-Jordan on the 8x8 pivot block A11, in registers
 //        (LPM/8 lanes per row, pivot rows exchanged by shuffles):
-//        X * A11 = c * I  with  X = diag(Z_{<j}) * E,  c = prod z_s,
+//        X * A11 = c * I  with  c = prod z_s: the pivot row of step s is scaled by
+//        lambda_s = z_0..z_{s-1} (the others by z_s), so every row ends up scaled
+//        by c and the in-place inverse part E is X itself;
 //        det(A11) = prod_s z_s^(s+1) / prod_s z_s^7
 //     M  one delayed pass  negM = -X * A12           (8 MACs, one REDC per element)
 //     T  trailing update   A22 <- c*A22 + A21*negM   (9 MACs, one REDC per element)
@@ -615,18 +617,20 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         uint32_t prow[EPL];
 #pragma unroll
         for (int k = 0; k < EPL; ++k) prow[k] = __shfl_sync(omask, v[k], s * LPR + l % LPR, LPM);
-        // Row s keeps its values (its prow is itself: 0 * v + 1 * v) and takes lam
-        // at column s; other rows: z v - t prow, with -t lam at column s.
+        // Other rows: z v - t prow, with -t lam at column s (the identity column of
+        // row s is lam there).  Row s is scaled by lam = prod_{t<s} z_t instead
+        // (lam * v; lam^2 at column s): then every row ends up scaled by c =
+        // prod z overall, so the in-place inverse part is X = c A11^-1 itself.
         const bool piv = pj == s;
         zl = piv ? lam : zl;
-        const uint32_t zz = piv ? 0u : z;
-        const uint32_t nn = piv ? one : p - t;   // p - t in (0, p]: a valid 2-product multiplier
+        const uint32_t zz = piv ? lam : z;
+        const uint32_t nn = piv ? 0u : p - t;   // p - t in (0, p]: a valid 2-product multiplier
 #pragma unroll
         for (int k = 0; k < EPL; ++k) {
           uint32_t a = v[k], b = prow[k];
           if (k == s % EPL) {   // the only element of this lane that can sit in column s
             const bool diag = pc == s - s % EPL;
-            a = diag ? 0u : a;
+            a = diag ? (piv ? lam : 0u) : a;
             b = diag ? lam : b;
           }
           v[k] = gj_red2(mad_wide(zz, a, mad_wide(nn, b, 0ull)), m);
@@ -647,12 +651,9 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       const uint32_t cR = lam;   // c = prod z_s
       Q = gj_mont(Q, cR, m);
       C = gj_mont(C, Q, m);
-      // negX = -Z_{<j} E  ->  NX[pj][pc + k]
+      // negX = -X  ->  NX[pj][pc + k]
 #pragma unroll
-      for (int k = 0; k < EPL; ++k) {
-        const uint32_t x = gj_mont(v[k], zl, m);
-        NX[gj_nx_row(pj) + pc + k] = x ? p - x : 0u;
-      }
+      for (int k = 0; k < EPL; ++k) NX[gj_nx_row(pj) + pc + k] = v[k] ? p - v[k] : 0u;
       __syncwarp(omask);
       // ---------------- M: negM = negX * A12, in place in the pivot rows ----------------
       if (PDB_GJ_ABL != 1) gj_mpass_any<LPM, P31>(A, NX, S, K, mrem, l, omask, m);
