@@ -639,13 +639,9 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         lam = gj_mont(lam, z, m);
       }
       if (lam == 0) { ok = false; break; }   // lam = prod z_s: zero iff a pivot vanished
-      {
-        // den *= lambda_1 ... lambda_6: row pj holds lambda_pj = zl; product over the rows
-        uint32_t f = (pj >= 1 && pj <= 6) ? zl : one;
-#pragma unroll
-        for (int d = LPR; d < LPM; d <<= 1) f = gj_mont(f, __shfl_xor_sync(omask, f, d, LPM), m);
-        den = gj_mont(den, f, m);
-      }
+      // den *= lambda_1 ... lambda_6: row pj holds lambda_pj = zl; each row's first
+      // lane keeps its factors, the lane group multiplies them together once per node
+      den = gj_mont(den, (pj >= 1 && pj <= 6 && l % LPR == 0) ? zl : one, m);
       num = gj_mont(num, z7, m);
       if (mrem == 0) break;
       const uint32_t cR = lam;   // c = prod z_s
@@ -662,6 +658,8 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       if (PDB_GJ_ABL != 2) gj_tpass_any<LPM, P31>(A, S, K, mrem, cR, l, m);
       __syncwarp(omask);
     }
+#pragma unroll
+    for (int d = 1; d < LPM; d <<= 1) den = gj_mont(den, __shfl_xor_sync(omask, den, d, LPM), m);
     if (l == 0) {
       if (ok) {
         // C^8
