@@ -22,6 +22,13 @@ executor.FORCE_MODE = "fused"
 run(m, cfg)
 executor.FORCE_MODE = "staged"
 run(m, cfg)
+import random  # noqa: E402
+from paper_2010_12117_b200 import poly_matrix  # noqa: E402
+rr = random.Random(1)
+for r in (16, 40):   # compile-time-order kernels with the dense DFT-8 fill (distinct entries)
+    rows = [[{(0,): rr.randint(-10**6, 10**6), (1,): rr.randint(-10**6, 10**6)} for _ in range(r)] for _ in range(r)]
+    executor.FORCE_MODE = "fused"
+    run(poly_matrix(rows, ("x",)))
 executor.FORCE_MODE = None
 run(*workloads.c1())
 m = workloads.c1()[0]
