@@ -26,6 +26,36 @@ __global__ void k_imadwide(uint32_t* out, uint32_t a0, uint32_t b0) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// loop-invariant operands: nothing but the accumulating IMAD.WIDE in the loop
+__global__ void k_imadwide_pure(uint32_t* out, uint32_t a0, uint32_t b0) {
+  uint32_t lo[ILP], hi[ILP], x[ILP];
+  const uint32_t y = b0 + threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) { lo[i] = i; hi[i] = 0; x[i] = (a0 ^ threadIdx.x) + i; }
+  LOOP(asm volatile("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.u32 %1, %2, %3, %1;" : "+r"(lo[i]), "+r"(hi[i]) : "r"(x[i]), "r"(y)));
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) s ^= lo[i] ^ hi[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// IMAD.WIDE interleaved 1:1 with IMAD.HI / with IMAD (loop-invariant operands)
+template <int KIND>
+__global__ void k_wide_plus(uint32_t* out, uint32_t a0, uint32_t b0) {
+  uint32_t lo[ILP], hi[ILP], x[ILP], z[ILP];
+  const uint32_t y = b0 + threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) { lo[i] = i; hi[i] = 0; x[i] = (a0 ^ threadIdx.x) + i; z[i] = i * 7; }
+  LOOP(asm volatile("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.u32 %1, %2, %3, %1;" : "+r"(lo[i]), "+r"(hi[i]) : "r"(x[i]), "r"(y));
+       if (KIND == 0) asm volatile("mad.hi.u32 %0, %0, %1, %0;" : "+r"(z[i]) : "r"(y));
+       else if (KIND == 1) asm volatile("mad.lo.u32 %0, %0, %1, %0;" : "+r"(z[i]) : "r"(y));
+       else asm volatile("add.u32 %0, %0, %1;" : "+r"(z[i]) : "r"(y)));
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) s ^= lo[i] ^ hi[i] ^ z[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void k_imadhi(uint32_t* out, uint32_t a0, uint32_t b0) {
   uint32_t v[ILP];
   const uint32_t y = b0 + threadIdx.x;
@@ -132,6 +162,10 @@ int main() {
            ops / (best * 1e-3) / (sms * (double)khz * 1e3));
   };
   run("imad.wide (acc)", k_imadwide);
+  run("imad.wide pure (loop-invariant operands)", k_imadwide_pure);
+  run("imad.wide + imad.hi pairs", k_wide_plus<0>);
+  run("imad.wide + imad pairs", k_wide_plus<1>);
+  run("imad.wide + iadd pairs (invariant operands)", k_wide_plus<2>);
   run("imad.hi", k_imadhi);
   run("imad.lo", k_imadlo);
   run("dfma", k_dfma);
