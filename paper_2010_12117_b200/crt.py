@@ -9,6 +9,7 @@ scalar API; `mrc_digits` reads the digits off the device-lifted value.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -127,8 +128,31 @@ def device_lift(residues_dev, primes, n: int, stride: int) -> list:
     sel = limbs.index_select(0, idx)[:, :width].contiguous()
     sel_neg = neg.index_select(0, idx)
     host = native.host_module()
-    return host.ints_from_limbs(np.ascontiguousarray(sel.cpu().numpy()), np.ascontiguousarray(idx.cpu().numpy()),
-                                np.ascontiguousarray(sel_neg.cpu().numpy()), int(n), int(width))
+    idx_h = np.ascontiguousarray(idx.cpu().numpy())
+    neg_h = np.ascontiguousarray(sel_neg.cpu().numpy())
+    with _PIN_LOCK:   # the staging buffer is shared; the ints are built before it is reused
+        return host.ints_from_limbs(_to_host(sel), idx_h, neg_h, int(n), int(width))
+
+
+_PINNED = {}
+_PIN_LOCK = threading.Lock()
+
+
+def _to_host(t):
+    """Device tensor -> numpy through a reused page-locked staging buffer (the
+    limb block of a large run is hundreds of MB; pageable copies run at a
+    fraction of the link rate).  Small tensors take the plain path."""
+    torch = native._torch()
+    nbytes = t.numel() * t.element_size()
+    if nbytes < (8 << 20) or t.device.type != "cuda":
+        return np.ascontiguousarray(t.cpu().numpy())
+    buf = _PINNED.get(t.device.index)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 28), dtype=torch.uint8, pin_memory=True)
+        _PINNED[t.device.index] = buf
+    view = buf[:nbytes].view(t.dtype).view(t.shape)
+    view.copy_(t)
+    return view.numpy()
 
 
 def mrc_digits(residues, basis: CrtBasis) -> list:
