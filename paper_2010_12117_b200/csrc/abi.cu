@@ -155,9 +155,14 @@ __global__ void peak_delayed(uint32_t* out, uint32_t seed, Mod32 m, int iters) {
 #pragma unroll
     for (int q = 0; q < 8; ++q)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i] += (uint64_t)tau[q] * (np[q] ^ i);
+      for (int i = 0; i < 4; ++i) acc[i] = mad_wide(tau[q], np[q] ^ i, acc[i]);
 #pragma unroll
     for (int i = 0; i < 4; ++i) a[i] = csub(csub(redc(acc[i], m), 2u * m.p), m.p);
+    // the multipliers depend on this iteration's results, so no product can be
+    // hoisted out of the loop (an earlier version let the compiler do exactly
+    // that and over-stated the peak)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tau[q] = a[q & 3] ^ q;
   }
   uint32_t s = 0;
 #pragma unroll

@@ -71,6 +71,10 @@ __global__ void k_tpass(uint32_t* out, uint32_t a0, uint32_t p, uint32_t qinv) {
       v = min(v, v - 2 * p);
       a[i] = min(v, v - p);
     }
+    // loop-carried multipliers: otherwise the compiler hoists the 32 products
+    // t[q] * (n[q] ^ i) out of the loop and the figure is meaningless
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = a[q & 3] ^ q;
   }
   uint32_t s = 0;
 #pragma unroll

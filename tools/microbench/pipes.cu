@@ -56,6 +56,49 @@ __global__ void k_wide_plus(uint32_t* out, uint32_t a0, uint32_t b0) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// one operand uniform (kernel parameter -> uniform register)
+__global__ void k_wide_uniform(uint32_t* out, uint32_t a0, uint32_t b0) {
+  uint32_t lo[ILP], hi[ILP], x[ILP];
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) { lo[i] = i; hi[i] = 0; x[i] = (a0 ^ threadIdx.x) + i; }
+  LOOP(asm volatile("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.u32 %1, %2, %3, %1;" : "+r"(lo[i]), "+r"(hi[i]) : "r"(x[i]), "r"(b0)));
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < ILP; ++i) s ^= lo[i] ^ hi[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// the trailing-update tile shape: acc[a][b] += x[a] * y[b], 2 x 4, x[a] shared by 4 consecutive MACs
+__global__ void k_wide_tile(uint32_t* out, uint32_t a0, uint32_t b0) {
+  uint32_t lo[2][4], hi[2][4], x[2][8], y[8][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) { lo[a][b] = a + b; hi[a][b] = 0; }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    x[0][q] = (a0 ^ threadIdx.x) + q; x[1][q] = (a0 ^ threadIdx.x) * 3 + q;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) y[q][b] = b0 + threadIdx.x * (b + 1) + q;
+  }
+  for (int it = 0; it < ITERS / 8; ++it) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          asm volatile("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.u32 %1, %2, %3, %1;"
+                       : "+r"(lo[a][b]), "+r"(hi[a][b]) : "r"(x[a][q]), "r"(y[q][b]));
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) s ^= lo[a][b] ^ hi[a][b];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void k_imadhi(uint32_t* out, uint32_t a0, uint32_t b0) {
   uint32_t v[ILP];
   const uint32_t y = b0 + threadIdx.x;
@@ -163,6 +206,8 @@ int main() {
   };
   run("imad.wide (acc)", k_imadwide);
   run("imad.wide pure (loop-invariant operands)", k_imadwide_pure);
+  run("imad.wide, one operand uniform", k_wide_uniform);
+  run("imad.wide 2x4 tile pattern (x[a] shared by 4 MACs)", k_wide_tile);
   run("imad.wide + imad.hi pairs", k_wide_plus<0>);
   run("imad.wide + imad pairs", k_wide_plus<1>);
   run("imad.wide + iadd pairs (invariant operands)", k_wide_plus<2>);
