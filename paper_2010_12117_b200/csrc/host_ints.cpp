@@ -6,10 +6,10 @@
 // into Python ints one `int.from_bytes` call at a time costs ~0.3-0.7 us each
 // in the interpreter.  This module does the same conversion in one C loop
 // (PyLong from the limb bytes, negated where the sign byte is set), writing
-// into a list pre-filled with the shared small int 0.
+// the coefficient tuple directly, zeros as the shared small int 0.
 //
 //   ints_from_limbs(limbs: bytes-like [count][width] u32, index: bytes-like int64[count],
-//                   neg: bytes-like uint8[count], n: int) -> list[int] of length n
+//                   neg: bytes-like uint8[count], n: int, width: int) -> tuple[int] of length n
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
 #include <cstdint>
@@ -51,67 +51,82 @@ static PyObject* long_from_limbs(const unsigned char* row, Py_ssize_t width, boo
 }
 #endif
 
+// One coefficient: |value| as `width` little-endian u32 limbs, then the sign.
+static PyObject* make_int(const unsigned char* row, Py_ssize_t width, bool negative) {
+#ifdef PDB_DIRECT_LONG
+  if (width <= 74) return long_from_limbs(row, width, negative);
+#endif
+  PyObject* v;
+  if (width <= 2) {
+    uint64_t mag = 0;
+    std::memcpy(&mag, row, (size_t)width * 4);
+    v = PyLong_FromUnsignedLongLong(mag);
+  } else {
+    v = _PyLong_FromByteArray(row, (size_t)width * 4, /*little_endian=*/1, /*is_signed=*/0);
+  }
+  if (v && negative) {
+    PyObject* m = PyNumber_Negative(v);
+    Py_DECREF(v);
+    v = m;
+  }
+  return v;
+}
+
 static PyObject* ints_from_limbs(PyObject*, PyObject* args) {
   Py_buffer limbs, index, neg;
   Py_ssize_t n, width;
   if (!PyArg_ParseTuple(args, "y*y*y*nn", &limbs, &index, &neg, &n, &width)) return nullptr;
   PyObject* out = nullptr;
   const Py_ssize_t count = index.len / (Py_ssize_t)sizeof(int64_t);
-  if (width < 1 || limbs.len != count * width * 4 || neg.len != count) {
+  const unsigned char* lb = static_cast<const unsigned char*>(limbs.buf);
+  const int64_t* ix = static_cast<const int64_t*>(index.buf);
+  const uint8_t* ng = static_cast<const uint8_t*>(neg.buf);
+  bool sorted = true;
+  PyObject* zero = nullptr;
+  if (width < 1 || n < 0 || limbs.len != count * width * 4 || neg.len != count) {
     PyErr_SetString(PyExc_ValueError, "ints_from_limbs: inconsistent buffer sizes");
     goto done;
   }
-  out = PyList_New(n);
+  for (Py_ssize_t j = 0; j < count; ++j) {
+    if (ix[j] < 0 || ix[j] >= n) {
+      PyErr_SetString(PyExc_IndexError, "ints_from_limbs: index out of range");
+      goto done;
+    }
+    if (j && ix[j] <= ix[j - 1]) sorted = false;
+  }
+  // the result is the coefficient tuple itself (CoeffTensor.coeffs), built in one pass
+  out = PyTuple_New(n);
   if (!out) goto done;
-  {
-    PyObject* zero = PyLong_FromLong(0);
+  zero = PyLong_FromLong(0);
+  if (sorted) {
+    Py_ssize_t j = 0;
+    for (Py_ssize_t i = 0; i < n; ++i) {
+      PyObject* v;
+      if (j < count && ix[j] == i) {
+        v = make_int(lb + (size_t)j * (size_t)width * 4, width, ng[j] != 0);
+        ++j;
+        if (!v) { Py_CLEAR(out); goto done; }
+      } else {
+        Py_INCREF(zero);
+        v = zero;
+      }
+      PyTuple_SET_ITEM(out, i, v);
+    }
+  } else {   // any order (duplicates: the last wins), before the tuple escapes
     for (Py_ssize_t i = 0; i < n; ++i) {
       Py_INCREF(zero);
-      PyList_SET_ITEM(out, i, zero);
+      PyTuple_SET_ITEM(out, i, zero);
     }
-    Py_DECREF(zero);
-    const unsigned char* lb = static_cast<const unsigned char*>(limbs.buf);
-    const int64_t* ix = static_cast<const int64_t*>(index.buf);
-    const uint8_t* ng = static_cast<const uint8_t*>(neg.buf);
     for (Py_ssize_t j = 0; j < count; ++j) {
-      const int64_t pos = ix[j];
-      if (pos < 0 || pos >= n) {
-        PyErr_SetString(PyExc_IndexError, "ints_from_limbs: index out of range");
-        Py_CLEAR(out);
-        goto done;
-      }
-      const unsigned char* row = lb + (size_t)j * (size_t)width * 4;
-      PyObject* v;
-#ifdef PDB_DIRECT_LONG
-      if (width <= 74) {
-        v = long_from_limbs(row, width, ng[j] != 0);
-        if (!v) { Py_CLEAR(out); goto done; }
-        PyObject* old = PyList_GET_ITEM(out, pos);
-        PyList_SET_ITEM(out, pos, v);
-        Py_DECREF(old);
-        continue;
-      }
-#endif
-      if (width <= 2) {
-        uint64_t mag = 0;
-        std::memcpy(&mag, row, (size_t)width * 4);
-        v = PyLong_FromUnsignedLongLong(mag);
-      } else {
-        v = _PyLong_FromByteArray(row, (size_t)width * 4, /*little_endian=*/1, /*is_signed=*/0);
-      }
+      PyObject* v = make_int(lb + (size_t)j * (size_t)width * 4, width, ng[j] != 0);
       if (!v) { Py_CLEAR(out); goto done; }
-      if (ng[j]) {
-        PyObject* m = PyNumber_Negative(v);
-        Py_DECREF(v);
-        if (!m) { Py_CLEAR(out); goto done; }
-        v = m;
-      }
-      PyObject* old = PyList_GET_ITEM(out, pos);
-      PyList_SET_ITEM(out, pos, v);
+      PyObject* old = PyTuple_GET_ITEM(out, ix[j]);
+      PyTuple_SET_ITEM(out, ix[j], v);
       Py_DECREF(old);
     }
   }
 done:
+  Py_XDECREF(zero);
   PyBuffer_Release(&limbs);
   PyBuffer_Release(&index);
   PyBuffer_Release(&neg);
@@ -120,7 +135,7 @@ done:
 
 static PyMethodDef methods[] = {
     {"ints_from_limbs", ints_from_limbs, METH_VARARGS,
-     "ints_from_limbs(limbs, index, neg, n, width) -> list of n Python ints"},
+     "ints_from_limbs(limbs, index, neg, n, width) -> tuple of n Python ints"},
     {nullptr, nullptr, 0, nullptr}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_pdb_host", "native result materialisation", -1, methods};

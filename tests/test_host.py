@@ -207,7 +207,11 @@ def test_native_ints_from_limbs_matches_python_path():
         want = limbs_to_ints(limbs, neg)
         keep = np.flatnonzero(limbs.any(axis=1))
         got = h.ints_from_limbs(limbs[keep].tobytes(), keep.astype(np.int64).tobytes(), neg[keep].tobytes(), n, L)
-        assert got == want
+        assert type(got) is tuple and list(got) == want
+        shuffled = rng.permutation(keep)                 # unsorted indices take the second loop
+        got2 = h.ints_from_limbs(limbs[shuffled].tobytes(), shuffled.astype(np.int64).tobytes(),
+                                 neg[shuffled].tobytes(), n, L)
+        assert got2 == got
         assert all(type(v) is int for v in got)
         zero = 0
         assert all(v is zero for v in got if v == 0)   # small ints stay the shared singletons
