@@ -33,9 +33,13 @@
 //
 // Shape choices measured on B200 (profiles/README_r01.md): 16 lanes per matrix
 // (two matrices per warp), 8 warps per CTA, 2 CTAs per SM (shared memory holds
-// 32 matrices of 40x40); 2x4 register tiles in the M and T passes (larger tiles
-// spill at the 128-register budget); matrix stride 16 (mod 32) words and
-// swizzled 8-word tiles against bank conflicts.
+// 32 matrices of 40x40); 2x4 register tiles in the M and T passes (2x8, 4x4
+// measured slower); matrix stride 16 (mod 32) words and swizzled 8-word tiles
+// against bank conflicts.  Padded orders 40 and 16 are also built with the
+// order as a template constant (RPC): the block loop unrolls and every
+// shared-memory address becomes an immediate offset (+10 %).  The kernel is
+// bound by the issue of IMAD.WIDE / IMAD.HI (~4 cycles per warp instruction
+// each on B200); see DESIGN.md section 4 for the per-phase cost model.
 #pragma once
 #include "pdb_internal.cuh"
 #include "dft8.cuh"
