@@ -41,6 +41,8 @@
 // bound by the issue of IMAD.WIDE / IMAD.HI (~4 cycles per warp instruction
 // each on B200); see DESIGN.md section 4 for the per-phase cost model.
 #pragma once
+#include <type_traits>
+
 #include "pdb_internal.cuh"
 #include "dft8.cuh"
 
@@ -394,9 +396,9 @@ __device__ __forceinline__ void gj_st_sw(uint32_t* a, int sw, const uint32_t (&v
 
 // P31: 2^30 <= p < 2^31 -- at most two products per reduction (2 p^2 < 2^63 keeps
 // hi(acc) + p < 2^32); the partial results are summed mod p.
-template <int TR, int TC, int LPM, bool P31>
+template <int TR, int TC, int LPM, bool P31, int B = GJ_B>
 __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, uint32_t cR, int l, const Mod32& m) {
-  const int c0 = K + GJ_B;
+  const int c0 = K + B;
   const int ntc = mrem / TC;
   const int tiles = (mrem / TR) * ntc;
   const uint32_t* npr = A + K * S;    // negM rows K..K+7
@@ -409,12 +411,12 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
     // distinct bank groups; column v of this lane's tile is physical column
     // cc + ((v + sw) mod 8).
     const int sw = (TC == 8 && (ti & 1)) ? 4 : 0;
-    uint32_t a21[TR][GJ_B];
+    uint32_t a21[TR][B];
     uint64_t acc[TR][TC];
 #pragma unroll
     for (int a = 0; a < TR; ++a) {
       const uint32_t* row = A + (i0 + a) * S;
-      gj_ld<GJ_B>(row + K, a21[a]);
+      gj_ld<B>(row + K, a21[a]);
       uint32_t v[TC];
       gj_ld_sw<TC>(row + cc, sw, v);
 #pragma unroll
@@ -422,7 +424,7 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
     }
     uint32_t sum[TR][TC];
 #pragma unroll
-    for (int q = 0; q < GJ_B; ++q) {
+    for (int q = 0; q < B; ++q) {
       uint32_t nm[TC];
       gj_ld_sw<TC>(npr + q * S + cc, sw, nm);
 #pragma unroll
@@ -431,7 +433,7 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
         for (int b = 0; b < TC; ++b) {
           const bool fresh = P31 && (q & 1);                   // q = 1, 3, 5, 7 open a new pair
           acc[a][b] = mad_wide(a21[a][q], nm[b], fresh ? 0ull : acc[a][b]);
-          if (P31 && (q % 2 == 0 || q == GJ_B - 1)) {         // fold after q = 0, 2, 4, 6, 7
+          if (P31 && (q % 2 == 0 || q == B - 1)) {         // fold after q = 0, 2, 4, ..., B-1
             const uint32_t v = gj_red2(acc[a][b], m);
             sum[a][b] = q == 0 ? v : add_mod(sum[a][b], v, m.p);
           }
@@ -449,7 +451,7 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
   }
 }
 
-template <int LPM, bool P31>
+template <int LPM, bool P31, int B = GJ_B>
 __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem, uint32_t cR, int l, const Mod32& m) {
   // largest tile that keeps >= ~70 % of the lanes busy
   // fraction of lane slots busy >= pct/100, in integers
@@ -466,11 +468,11 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
 #ifndef PDB_GJ_T44
 #define PDB_GJ_T44 0   // 4x4 trailing tiles (experiment)
 #endif
-  if (PDB_GJ_T28 && minb < 4 && util(2, 8, 70)) gj_tpass<2, 8, LPM, P31>(A, S, K, mrem, cR, l, m);
-  else if (PDB_GJ_T44 && util(4, 4, 70)) gj_tpass<4, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
-  else if (util(2, 4, 70)) gj_tpass<2, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
-  else if (util(1, 4, 70)) gj_tpass<1, 4, LPM, P31>(A, S, K, mrem, cR, l, m);
-  else gj_tpass<1, 2, LPM, P31>(A, S, K, mrem, cR, l, m);
+  if (PDB_GJ_T28 && minb < 4 && util(2, 8, 70)) gj_tpass<2, 8, LPM, P31, B>(A, S, K, mrem, cR, l, m);
+  else if (PDB_GJ_T44 && util(4, 4, 70)) gj_tpass<4, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
+  else if (util(2, 4, 70)) gj_tpass<2, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
+  else if (util(1, 4, 70)) gj_tpass<1, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
+  else gj_tpass<1, 2, LPM, P31, B>(A, S, K, mrem, cR, l, m);
 }
 
 // ---- M pass: negM[j][c] = sum_q negX[j][q] A12[q][c], in place in pivot rows K..K+7 ----
@@ -478,24 +480,24 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
 // block of A12 and RPI rows of negX (16 B loads) for RPI*TC*8 MACs.  Items are
 // numbered column-group major, so the lanes sharing a column group work in the
 // same pass; they read it completely before any of them overwrites it.
-template <int RPI, int TC, int LPM, bool P31>
+template <int RPI, int TC, int LPM, bool P31, int B = GJ_B>
 __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S, int K, int mrem, int l,
                                          unsigned omask, const Mod32& m) {
-  constexpr int NRG = GJ_B / RPI;
+  constexpr int NRG = B / RPI;
   const int items = (mrem / TC) * NRG;
   for (int w0 = 0; w0 < items; w0 += LPM) {
     const int w = w0 + l;
     const bool act = w < items;
     const int cg = w / NRG, rg = w - (w / NRG) * NRG;
-    const int c = K + GJ_B + TC * cg;
+    const int c = K + B + TC * cg;
     uint32_t res[RPI][TC];
     if (act) {
-      uint32_t x[RPI][GJ_B];   // this item's negX rows, 16 B loads
+      uint32_t x[RPI][B];   // this item's negX rows, 16 B loads
 #pragma unroll
-      for (int t = 0; t < RPI; ++t) gj_ld<GJ_B>(NX + gj_nx_row(rg * RPI + t), x[t]);
+      for (int t = 0; t < RPI; ++t) gj_ld<B>(NX + gj_nx_row(rg * RPI + t), x[t]);
       uint64_t acc[RPI][TC];
 #pragma unroll
-      for (int q = 0; q < GJ_B; ++q) {
+      for (int q = 0; q < B; ++q) {
         uint32_t a[TC];
         gj_ld<TC>(A + (K + q) * S + c, a);
 #pragma unroll
@@ -525,22 +527,22 @@ __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S,
   }
 }
 
-template <int LPM, bool P31>
+template <int LPM, bool P31, int B = GJ_B>
 __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, int S, int K, int mrem, int l,
                                              unsigned omask, const Mod32& m) {
   auto util = [&](int rpi, int tc, int pct) {
-    const int t = (mrem / tc) * (GJ_B / rpi);
+    const int t = (mrem / tc) * (B / rpi);
     return 100 * t >= pct * ((t + LPM - 1) / LPM) * LPM;
   };
 #ifndef PDB_GJ_M44
 #define PDB_GJ_M44 0   // 4x4 M-pass tiles (measured slower than 2x4 at 128 registers)
 #endif
-  if (PDB_GJ_M44 && util(4, 4, 74)) gj_mpass<4, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(2, 4, 74)) gj_mpass<2, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(4, 2, 74)) gj_mpass<4, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(1, 4, 74)) gj_mpass<1, 4, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
-  else if (util(2, 2, 74)) gj_mpass<2, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
-  else gj_mpass<1, 2, LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+  if (PDB_GJ_M44 && util(4, 4, 74)) gj_mpass<4, 4, LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(2, 4, 74)) gj_mpass<2, 4, LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(4, 2, 74)) gj_mpass<4, 2, LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(1, 4, 74)) gj_mpass<1, 4, LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
+  else if (util(2, 2, 74)) gj_mpass<2, 2, LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
+  else gj_mpass<1, 2, LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
 }
 
 // ---- the kernel ------------------------------------------------------------------------------
@@ -557,8 +559,16 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
               unsigned long long* __restrict__ flag_count, int64_t* __restrict__ flag_nodes, GjGeom g, Mod32 m) {
   static_assert(LPM == 8 || LPM == 16 || LPM == 32, "8, 16 or 32 lanes per matrix");
   static_assert(RPC % GJ_B == 0, "compile-time order must be padded to the block size");
-  constexpr int LPR = LPM / 8;   // lanes per pivot-block row
-  constexpr int EPL = 8 / LPR;   // pivot-block elements per lane
+  // Pivot-block schedule: blocks of 8, except that the staged compile-time
+  // order-40 kernel (p < 2^30, 16 lanes) eliminates its last 8 columns as two
+  // blocks of 4 (a 4x4 Gauss-Jordan costs a third of an 8x8 one per column; the
+  // last block has no trailing update to pay for it).  Measured
+  // (profiles/README_r01.md): staged r = 40 +2 %, but the fused kernel is
+  // fastest with blocks of 8 throughout, so it keeps them.
+#ifndef PDB_GJ_TAIL4
+#define PDB_GJ_TAIL4 8
+#endif
+  constexpr int TAIL4 = (RPC == 40 && !P31 && LPM == 16 && !DFT8) ? PDB_GJ_TAIL4 : 0;
   extern __shared__ __align__(16) uint32_t smem[];
   const int r = g.r;
   const int RP = RPC ? RPC : g.RP;
@@ -573,7 +583,6 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
   uint32_t* A = mats + (size_t)slot * MS;
   uint32_t* NX = A + RP * S;          // negX [8][8]
   const uint32_t p = m.p, one = m.r1;
-  const int pj = l / LPR, pc = EPL * (l % LPR);   // my pivot-block row / first column
 
   const int64_t iters = DFT8 ? (nodes / g.M) : (nodes + g.M - 1) / g.M;
   bool dense;   // identity entry ids and no padding: affine fills
@@ -601,11 +610,18 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
     else node = gj_node_linear(it, slot, g, nodes);
     if (node < 0) continue;
 
-    uint32_t num = one, den = one, Q = one, C = one;
-    bool ok = true;
-#pragma unroll
-    for (int K = 0; K < RP; K += GJ_B) {
-      const int mrem = RP - K - GJ_B;
+    // C8 / C4: products of the running c-prefix Q taken before each block of 8 / 4
+    // (det A picks up Q^B per block: den *= C8^8 C4^4 at the end)
+    uint32_t num = one, den = one, Q = one, C8 = one, C4 = one;
+
+    // One block of B pivots at column K; false if a pivot vanished.
+    auto block = [&](auto Bc, int K) -> bool {
+      constexpr int B = decltype(Bc)::value;
+      constexpr int LPR = LPM / B;   // lanes per pivot-block row
+      constexpr int EPL = B / LPR;   // pivot-block elements per lane
+      static_assert(EPL >= 1, "block narrower than the lane group");
+      const int pj = l / LPR, pc = EPL * (l % LPR);   // my pivot-block row / first column
+      const int mrem = RP - K - B;
       // ---------------- P: Gauss-Jordan on the pivot block ----------------
       uint32_t v[EPL];
       {
@@ -613,9 +629,9 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
 #pragma unroll
         for (int k = 0; k < EPL; ++k) v[k] = src_row[k];
       }
-      uint32_t lam = one, zl = one, z7 = one;
+      uint32_t lam = one, zl = one, zlast = one;
 #pragma unroll
-      for (int s = 0; s < GJ_B; ++s) {
+      for (int s = 0; s < B; ++s) {
         const uint32_t z = __shfl_sync(omask, v[s % EPL], s * LPR + s / EPL, LPM);
         const uint32_t t = __shfl_sync(omask, v[s % EPL], pj * LPR + s / EPL, LPM);
         uint32_t prow[EPL];
@@ -639,39 +655,60 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
           }
           v[k] = gj_red2(mad_wide(zz, a, mad_wide(nn, b, 0ull)), m);
         }
-        if (s == GJ_B - 1) z7 = z;
+        if (s == B - 1) zlast = z;
         lam = gj_mont(lam, z, m);
       }
-      if (lam == 0) { ok = false; break; }   // lam = prod z_s: zero iff a pivot vanished
-      // den *= lambda_1 ... lambda_6: row pj holds lambda_pj = zl; each row's first
-      // lane keeps its factors, the lane group multiplies them together once per node
-      den = gj_mont(den, (pj >= 1 && pj <= 6 && l % LPR == 0) ? zl : one, m);
-      num = gj_mont(num, z7, m);
-      if (mrem == 0) break;
+      if (lam == 0) return false;   // lam = prod z_s: zero iff a pivot vanished
+      // det(A11) = z_{B-1} / (lambda_1 ... lambda_{B-2}): row pj holds lambda_pj = zl;
+      // each row's first lane keeps its factors, the group multiplies them once per node
+      den = gj_mont(den, (pj >= 1 && pj <= B - 2 && l % LPR == 0) ? zl : one, m);
+      num = gj_mont(num, zlast, m);
+      if (mrem == 0) return true;
       const uint32_t cR = lam;   // c = prod z_s
       Q = gj_mont(Q, cR, m);
-      C = gj_mont(C, Q, m);
+      if (K + B < RP - TAIL4) C8 = gj_mont(C8, Q, m);   // the next block has 8 pivots
+      else C4 = gj_mont(C4, Q, m);
       // negX = -X  ->  NX[pj][pc + k]
 #pragma unroll
       for (int k = 0; k < EPL; ++k) NX[gj_nx_row(pj) + pc + k] = v[k] ? p - v[k] : 0u;
       __syncwarp(omask);
       // ---------------- M: negM = negX * A12, in place in the pivot rows ----------------
-      if (PDB_GJ_ABL != 1) gj_mpass_any<LPM, P31>(A, NX, S, K, mrem, l, omask, m);
+      if (PDB_GJ_ABL != 1) gj_mpass_any<LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
       __syncwarp(omask);
       // ---------------- T: trailing rows ----------------
-      if (PDB_GJ_ABL != 2) gj_tpass_any<LPM, P31>(A, S, K, mrem, cR, l, m);
+      if (PDB_GJ_ABL != 2) gj_tpass_any<LPM, P31, B>(A, S, K, mrem, cR, l, m);
       __syncwarp(omask);
+      return true;
+    };
+
+    bool ok = true;
+    if constexpr (TAIL4 > 0) {
+      // RPC = 40: 8 8 8 8 | 4 4 (TAIL4 = 8) -- every K and block size a constant
+      constexpr int K8 = RPC - TAIL4;
+      static_assert(K8 % GJ_B == 0 && TAIL4 % 4 == 0, "tail split");
+#pragma unroll
+      for (int K = 0; K < K8; K += 8)
+        if (ok && !block(std::integral_constant<int, 8>{}, K)) ok = false;
+#pragma unroll
+      for (int K = K8; K < RPC; K += 4)
+        if (ok && !block(std::integral_constant<int, 4>{}, K)) ok = false;
+    } else {
+#pragma unroll
+      for (int K = 0; K < RP; K += GJ_B)
+        if (!block(std::integral_constant<int, GJ_B>{}, K)) { ok = false; break; }
     }
 #pragma unroll
     for (int d = 1; d < LPM; d <<= 1) den = gj_mont(den, __shfl_xor_sync(omask, den, d, LPM), m);
     if (l == 0) {
       if (ok) {
-        // C^8
-        C = gj_mont(C, C, m);
-        C = gj_mont(C, C, m);
-        C = gj_mont(C, C, m);
+        uint32_t c = C8;   // C8^8 * C4^4
+#pragma unroll
+        for (int i = 0; i < 3; ++i) c = gj_mont(c, c, m);
+        uint32_t c4 = C4;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) c4 = gj_mont(c4, c4, m);
         num_out[node] = num;
-        den_out[node] = gj_mont(den, C, m);
+        den_out[node] = gj_mont(den, gj_mont(c, c4, m), m);
       } else {
         den_out[node] = 0u;
         unsigned long long k = atomicAdd(flag_count, 1ull);
