@@ -491,3 +491,20 @@ def test_resume_reference_written_partial_workspace(cuda, tmp_path):
     again = []
     assert resume(ws, PipelineConfig(progress=again.append)).coeffs == got.coeffs
     assert again == []
+
+
+@pytest.mark.parametrize("r", [13, 16, 36, 40])
+def test_compile_time_and_runtime_order_kernels_agree(cuda, r, monkeypatch):
+    """Padded orders 16 and 40 run compile-time-order kernels (the staged
+    order-40 one with a 4-pivot tail); PDB_GJ_NO_RPC=1 selects the generic
+    runtime-order kernel.  Both equal the oracle, zero pivots included."""
+    spec = find_fourier_primes(8, 1, start=10**9, min_count=1)[0]
+    rng = np.random.default_rng(100 + r)
+    mats = rng.integers(0, spec.p, (300, r, r))
+    mats[::9, 0, 0] = 0
+    mats[4::13, r - 2, :] = 0
+    grids = [mats[:, e // r, e % r] for e in range(r * r)]
+    want = O.det_grid(grids, r, spec.p).tolist()
+    assert det_grid(grids, r, spec).tolist() == want
+    monkeypatch.setenv("PDB_GJ_NO_RPC", "1")
+    assert det_grid(grids, r, spec).tolist() == want
