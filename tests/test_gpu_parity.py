@@ -493,7 +493,7 @@ def test_resume_reference_written_partial_workspace(cuda, tmp_path):
     assert again == []
 
 
-@pytest.mark.parametrize("r", [13, 16, 36, 40])
+@pytest.mark.parametrize("r", [13, 16, 24, 36, 40])
 def test_compile_time_and_runtime_order_kernels_agree(cuda, r, monkeypatch):
     """Padded orders 16 and 40 run compile-time-order kernels (the staged
     order-40 one with a 4-pivot tail); PDB_GJ_NO_RPC=1 selects the generic
