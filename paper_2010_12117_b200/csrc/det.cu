@@ -114,76 +114,123 @@ det_robust(Src src, const int32_t* __restrict__ ids, int r, const int64_t* __res
 }
 
 // ----------------------------------------------------------------- small ----
+// One lane per matrix, D matrices per lane (D = 4 for r <= 4, 2 for r <= 6):
+// the entries are read as Montgomery forms of A' = A R^-1 (no conversion), the
+// division-free elimination row_i <- z row_i - t row_k is one REDC of two
+// products, and the D x 32 inflations of a warp share one Fermat inversion
+// (prefix products within the lane, then across the warp by shuffles).
+// det A = det A' * R^r is applied by the last Montgomery product (Rr = R^r).
+// Valid for odd p < 2^31: two products < 2 p^2 keep REDC's bound and its
+// output below 2p, one conditional subtraction makes it canonical.
 template <int R, class Src>
 __global__ void __launch_bounds__(128)
 det_small(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t nodes,
-          uint32_t* __restrict__ out, FlagList flags, Mod32 m) {
+          uint32_t* __restrict__ out, FlagList flags, Mod32 m, uint32_t Rr) {
+#ifndef PDB_SMALL_D4
+#define PDB_SMALL_D4 4
+#endif
+  constexpr int D = R <= 4 ? PDB_SMALL_D4 : (R <= 6 ? 2 : 1);
   __shared__ int32_t ids[R * R];
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) ids[e] = ids_g[e];
   __syncthreads();
-  const uint32_t p = m.p;
+  const uint32_t p = m.p, one = m.r1;
   const int lane = threadIdx.x & 31;
   // warp-uniform trip count: every lane takes part in the batched inversion
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < nodes; base += stride) {
-    const int64_t idx = base + lane;
-    const bool valid = idx < nodes;
-    const int64_t node = node_lo + (valid ? idx : 0);
-    uint32_t a[R][R];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * D;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * D; base < nodes; base += stride) {
+    uint32_t a[D][R][R];
 #pragma unroll
-    for (int i = 0; i < R; ++i)
+    for (int d = 0; d < D; ++d) {
+      const int64_t idx = base + d * 32 + lane;
+      const int64_t node = node_lo + (idx < nodes ? idx : 0);
 #pragma unroll
-      for (int j = 0; j < R; ++j) a[i][j] = src.get(ids[i * R + j], node);
-    uint32_t preR = m.r1, inflR = m.r1;   // Montgomery forms
-    bool ok = true;
+      for (int i = 0; i < R; ++i)
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const uint32_t z = a[k][k];
-      ok = ok && z != 0;
-      const uint32_t zR = to_mont(z, m);
-      preR = mont(preR, zR, m);
-      if (k + 1 < R) inflR = mont(inflR, preR, m);
+        for (int j = 0; j < R; ++j) a[d][i][j] = src.get(ids[i * R + j], node);
+    }
+    uint32_t pre[D], infl[D];
+    bool ok[D];
 #pragma unroll
-      for (int i = k + 1; i < R; ++i) {
-        // row_i <- z*row_i - t*row_k  as one REDC of two 64-bit products
-        const uint32_t tR = to_mont(a[i][k], m);
-        const uint32_t ntR = tR ? p - tR : 0u;
+    for (int d = 0; d < D; ++d) {
+      pre[d] = one;
+      infl[d] = one;
+      ok[d] = true;
 #pragma unroll
-        for (int j = k + 1; j < R; ++j)
-          a[i][j] = canon32(redc(mad_wide(a[k][j], ntR, mad_wide(a[i][j], zR, 0ull)), m), m);
+      for (int k = 0; k < R; ++k) {
+        const uint32_t z = a[d][k][k];
+        ok[d] = ok[d] && z != 0;
+        pre[d] = gj_mont(pre[d], z, m);
+        if (k + 1 < R) infl[d] = gj_mont(infl[d], pre[d], m);
+#pragma unroll
+        for (int i = k + 1; i < R; ++i) {
+          const uint32_t nt = p - a[d][i][k];   // in (0, p]
+#pragma unroll
+          for (int j = k + 1; j < R; ++j)
+            a[d][i][j] = gj_red2(mad_wide(a[d][k][j], nt, mad_wide(a[d][i][j], z, 0ull)), m);
+        }
       }
     }
-    // Montgomery batch inversion of the 32 inflations of this warp:
-    // prefix/suffix products by shuffles and a single Fermat exponentiation.
-    const bool use = valid && ok;
-    const uint32_t x = use ? inflR : m.r1;
-    uint32_t pre_x = x, suf_x = x;
+    // batched inversion: lane-local prefix products, then across the warp
+    uint32_t lp[D];
+    uint32_t run = one;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t up = __shfl_up_sync(0xffffffffu, pre_x, d);
-      const uint32_t dn = __shfl_down_sync(0xffffffffu, suf_x, d);
-      if (lane >= d) pre_x = mont(pre_x, up, m);
-      if (lane + d < 32) suf_x = mont(suf_x, dn, m);
+    for (int d = 0; d < D; ++d) {
+      const bool use = base + d * 32 + lane < nodes && ok[d];
+      run = gj_mont(run, use ? infl[d] : one, m);
+      lp[d] = run;
     }
-    const uint32_t totalR = __shfl_sync(0xffffffffu, pre_x, 31);
-    const uint32_t inv_totalR = mont_pow(totalR, (uint64_t)p - 2, m);
+    uint32_t pre_x = run, suf_x = run;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const uint32_t up = __shfl_up_sync(0xffffffffu, pre_x, k);
+      const uint32_t dn = __shfl_down_sync(0xffffffffu, suf_x, k);
+      if (lane >= k) pre_x = gj_mont(pre_x, up, m);
+      if (lane + k < 32) suf_x = gj_mont(suf_x, dn, m);
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, pre_x, 31);
+    uint32_t inv_total = one;   // total^(p-2), square and multiply
+    {
+      uint32_t b = total;
+      for (uint32_t e = p - 2; e; e >>= 1) {
+        if (e & 1) inv_total = gj_mont(inv_total, b, m);
+        b = gj_mont(b, b, m);
+      }
+    }
     uint32_t left = __shfl_up_sync(0xffffffffu, pre_x, 1);
     uint32_t right = __shfl_down_sync(0xffffffffu, suf_x, 1);
-    if (lane == 0) left = m.r1;
-    if (lane == 31) right = m.r1;
-    const uint32_t invR = mont(mont(left, right, m), inv_totalR, m);   // x^-1 * R
-    if (valid) {
-      if (ok) out[idx] = mont(mont(preR, invR, m), 1u, m);
-      else flag_node(flags, node);
+    if (lane == 0) left = one;
+    if (lane == 31) right = one;
+    uint32_t inv = gj_mont(gj_mont(left, right, m), inv_total, m);   // 1 / (this lane's product)
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) {
+      const int64_t idx = base + d * 32 + lane;
+      const bool valid = idx < nodes;
+      const bool use = valid && ok[d];
+      const uint32_t inv_d = d ? gj_mont(inv, lp[d - 1], m) : inv;   // 1 / infl[d]
+      if (use) inv = gj_mont(inv, infl[d], m);
+      if (valid) {
+        if (ok[d]) out[idx] = gj_mont(gj_mont(pre[d], inv_d, m), Rr, m);
+        else flag_node(flags, node_lo + idx);
+      }
     }
   }
+}
+
+// 2^(32 r) mod p: the Montgomery scale of an r x r determinant.
+static uint32_t mont_scale(const Mod32& m, int r) {
+  uint64_t acc = 1 % m.p, b = m.r1;
+  for (int e = r; e; e >>= 1) {
+    if (e & 1) acc = (uint64_t)((unsigned __int128)acc * b % m.p);
+    b = (uint64_t)((unsigned __int128)b * b % m.p);
+  }
+  return (uint32_t)acc;
 }
 
 template <class Src>
 static int launch_small(int r, Src src, const int32_t* ids, int64_t lo, int64_t n, uint32_t* out,
                         FlagList f, Mod32 m, int grid, cudaStream_t st) {
   switch (r) {
-#define PDB_SMALL(R) case R: det_small<R, Src><<<grid, 128, 0, st>>>(src, ids, lo, n, out, f, m); count_launch(); break;
+#define PDB_SMALL(R) case R: det_small<R, Src><<<grid, 128, 0, st>>>(src, ids, lo, n, out, f, m, mont_scale(m, R)); count_launch(); break;
     PDB_SMALL(1) PDB_SMALL(2) PDB_SMALL(3) PDB_SMALL(4)
     PDB_SMALL(5) PDB_SMALL(6) PDB_SMALL(7) PDB_SMALL(8)
 #undef PDB_SMALL
@@ -213,16 +260,6 @@ static void launch_robust(PrimeCtx* ctx, Src src, const int32_t* ids, int r, con
   det_robust<Src><<<grid, 32 * warps, smem, st>>>(src, ids, r, list, list_count, count, node_lo, out,
                                                   ctx->m, trail_vals, trail_cols);
   count_launch();
-}
-
-// 2^(32 r) mod p: the Montgomery scale of an r x r determinant.
-static uint32_t mont_scale(const Mod32& m, int r) {
-  uint64_t acc = 1 % m.p, b = m.r1;
-  for (int e = r; e; e >>= 1) {
-    if (e & 1) acc = (uint64_t)((unsigned __int128)acc * b % m.p);
-    b = (uint64_t)((unsigned __int128)b * b % m.p);
-  }
-  return (uint32_t)acc;
 }
 
 template <class Src, bool DFT8, int LPM, bool P31, int RPC>
@@ -307,7 +344,8 @@ int det_run(PrimeCtx* ctx, Src src, const int32_t* ids, int r, int64_t node_lo, 
   if (cudaMemsetAsync(flags.count, 0, sizeof(unsigned long long), st) != cudaSuccess)
     return check_launch("det memset");
   if (r <= 8 && m.odd()) {
-    int64_t blocks = (nodes + 127) / 128;
+    const int per_lane = r <= 4 ? PDB_SMALL_D4 : (r <= 6 ? 2 : 1);   // det_small's D
+    int64_t blocks = (nodes + 128 * per_lane - 1) / (128 * per_lane);
     int grid = (int)(blocks < (int64_t)ctx->sms * 32 ? blocks : (int64_t)ctx->sms * 32);
     launch_small(r, src, ids, node_lo, nodes, out, flags, m, grid, st);
     fast = true;
