@@ -560,15 +560,18 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
   static_assert(LPM == 8 || LPM == 16 || LPM == 32, "8, 16 or 32 lanes per matrix");
   static_assert(RPC % GJ_B == 0, "compile-time order must be padded to the block size");
   // Pivot-block schedule: blocks of 8, except that the staged compile-time
-  // order-40 kernel (p < 2^30, 16 lanes) eliminates its last 8 columns as two
-  // blocks of 4 (a 4x4 Gauss-Jordan costs a third of an 8x8 one per column; the
-  // last block has no trailing update to pay for it).  Measured
-  // (profiles/README_r01.md): staged r = 40 +2 %, but the fused kernel is
-  // fastest with blocks of 8 throughout, so it keeps them.
+  // kernels (orders 40 and 16, p < 2^30, 16 lanes) eliminate their last 8
+  // columns as two blocks of 4 (a 4x4 Gauss-Jordan costs a third of an 8x8 one
+  // per column; the last block has no trailing update to pay for it).
+  // Measured (profiles/README_r01.md): staged r = 40 +2 %, r = 16 +3.5 %; the
+  // fused kernel is fastest with blocks of 8 throughout, so it keeps them.
 #ifndef PDB_GJ_TAIL4
 #define PDB_GJ_TAIL4 8
 #endif
-  constexpr int TAIL4 = (RPC == 40 && !P31 && LPM == 16 && !DFT8) ? PDB_GJ_TAIL4 : 0;
+#ifndef PDB_GJ_TAIL4_16
+#define PDB_GJ_TAIL4_16 8
+#endif
+  constexpr int TAIL4 = (!P31 && LPM == 16 && !DFT8) ? (RPC == 40 ? PDB_GJ_TAIL4 : (RPC == 16 ? PDB_GJ_TAIL4_16 : 0)) : 0;
   extern __shared__ __align__(16) uint32_t smem[];
   const int r = g.r;
   const int RP = RPC ? RPC : g.RP;
@@ -683,7 +686,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
 
     bool ok = true;
     if constexpr (TAIL4 > 0) {
-      // RPC = 40: 8 8 8 8 | 4 4 (TAIL4 = 8) -- every K and block size a constant
+      // e.g. RPC = 40: 8 8 8 8 | 4 4 (TAIL4 = 8) -- every K and block size a constant
       constexpr int K8 = RPC - TAIL4;
       static_assert(K8 % GJ_B == 0 && TAIL4 % 4 == 0, "tail split");
 #pragma unroll
