@@ -293,14 +293,21 @@ static int launch_gj_mode(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int
                          uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
   // 16 lanes per matrix (the measured best for every order); 2^30 <= p < 2^31 reduces pairs of products
   const GjGeom g = gj_pick(r, PDB_GJ_LANES, DFT8);
-  // compile-time orders for the common sizes (C5: 40, C3/C4: 16); those kernels
-  // assume 256-thread CTAs
-  const bool rpc = g.M * PDB_GJ_LANES == 256 && !getenv("PDB_GJ_NO_RPC");
+  // compile-time orders: 40 (C5) and 16 (C3/C4) for both sources, 24 and 32 for
+  // staged grids; the fused DFT-8 fill of the compile-time kernels assumes
+  // 256-thread CTAs, the staged ones take any CTA size
+  const bool rpc = (!DFT8 || g.M * PDB_GJ_LANES == 256) && !getenv("PDB_GJ_NO_RPC");
   if (ctx->m.fast()) {
     if (g.RP == 40 && rpc)
       return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 40>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
     if (g.RP == 16 && rpc)
       return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 16>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+    if constexpr (!DFT8) {
+      if (g.RP == 24 && rpc)
+        return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 24>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+      if (g.RP == 32 && rpc)
+        return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 32>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+    }
     return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 0>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
   }
   if (g.RP == 40 && rpc)

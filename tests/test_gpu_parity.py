@@ -493,10 +493,10 @@ def test_resume_reference_written_partial_workspace(cuda, tmp_path):
     assert again == []
 
 
-@pytest.mark.parametrize("r", [13, 16, 24, 36, 40])
+@pytest.mark.parametrize("r", [13, 16, 21, 24, 30, 32, 36, 40])
 def test_compile_time_and_runtime_order_kernels_agree(cuda, r, monkeypatch):
-    """Padded orders 16 and 40 run compile-time-order kernels (the staged
-    order-40 one with a 4-pivot tail); PDB_GJ_NO_RPC=1 selects the generic
+    """Padded orders 16, 24, 32 and 40 run compile-time-order kernels (the staged
+    16 and 40 ones with a 4-pivot tail); PDB_GJ_NO_RPC=1 selects the generic
     runtime-order kernel.  Both equal the oracle, zero pivots included."""
     spec = find_fourier_primes(8, 1, start=10**9, min_count=1)[0]
     rng = np.random.default_rng(100 + r)
