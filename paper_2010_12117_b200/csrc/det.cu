@@ -25,7 +25,7 @@
 #include "det_gj.cuh"
 
 #ifndef PDB_GJ_LANES
-#define PDB_GJ_LANES 16   // lanes per matrix (measured best at r = 10..40; 8 and 32 build for experiments)
+#define PDB_GJ_LANES 16   // lanes per matrix up to order 40 (see gj_lanes); 8 and 32 build for experiments
 #endif
 
 namespace pdb {
@@ -288,10 +288,24 @@ static int launch_gj_geom(PrimeCtx* ctx, const GjGeom& g, Src src, const int32_t
   return check_launch("det_gj_finalize");
 }
 
+// Lanes per matrix: 16 up to order 40 (measured sweep, r = 10..40) and at 56 / 64;
+// 32 at padded order 48 and from 72 on, where few matrices fit in shared memory
+// and more lanes per matrix hide latency (profiles/README_r01.md: r = 44 +33 %,
+// 96 +28 %, 128 +160 %; r = 64 -57 %, its 64-word rows share banks).
+static int gj_lanes(int r) {
+  const int RP = (r + 7) & ~7;
+  return (RP == 48 || RP >= 72) ? 32 : PDB_GJ_LANES;
+}
+
 template <class Src, bool DFT8>
 static int launch_gj_mode(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int64_t node_lo, int64_t nodes,
                          uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
-  // 16 lanes per matrix (the measured best for every order); 2^30 <= p < 2^31 reduces pairs of products
+  // 2^30 <= p < 2^31 (not fast) reduces pairs of products
+  if (gj_lanes(r) == 32 && PDB_GJ_LANES != 32) {
+    const GjGeom g = gj_pick(r, 32, DFT8);
+    if (ctx->m.fast()) return launch_gj_geom<Src, DFT8, 32, false, 0>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+    return launch_gj_geom<Src, DFT8, 32, true, 0>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
+  }
   const GjGeom g = gj_pick(r, PDB_GJ_LANES, DFT8);
   // compile-time orders: 40 (C5) and 16 (C3/C4) for both sources, 24 and 32 for
   // staged grids; the fused DFT-8 fill of the compile-time kernels assumes
@@ -324,7 +338,7 @@ static int launch_gj(PrimeCtx* ctx, int r, StagedSrc src, const int32_t* ids, in
 
 static int launch_gj(PrimeCtx* ctx, int r, FusedSrc src, const int32_t* ids, int64_t node_lo, int64_t nodes,
                      uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
-  const GjGeom g = gj_pick(r, PDB_GJ_LANES, true);
+  const GjGeom g = gj_pick(r, gj_lanes(r), true);
   const bool dft8 = src.E <= 8 && src.NL >= 8 && src.NL % (8 * g.U) == 0 && node_lo % src.NL == 0 &&
                     nodes % src.NL == 0;
   if (dft8) return launch_gj_mode<FusedSrc, true>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
