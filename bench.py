@@ -246,9 +246,16 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks: several ranks on one GPU (PDB_BENCH_DEVICE=0) with gloo for the
+    # barrier / max-over-ranks plumbing (PDB_DIST_BACKEND=gloo); defaults: NCCL, GPU = local rank
+    local = int(os.environ.get("PDB_BENCH_DEVICE", local))
+    backend = os.environ.get("PDB_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     m, pl = workload(args.config)
