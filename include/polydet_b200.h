@@ -84,6 +84,43 @@ int32_t pdb_eval_det_fused_u32(pdb_prime_ctx* ctx, const uint32_t* partial, int6
                                int64_t node_lo, int64_t nodes, uint32_t* out, void* scratch,
                                size_t scratch_bytes, void* stream);
 
+/* ---- pruned node sets (csrc/expand.cu) --------------------
+ * det(M) has degree <= D_a in variable a (the plan's degree bound,
+ * pipeline.py:184-196), so on an axis of N >= 16 nodes the determinants at the
+ * nodes u + (N/8) v with u < U, v < 8 (any U >= floor(D_a/8) + 1) determine
+ * the determinant at every node.  A node map names those kept nodes; kernels
+ * taking one index the kept nodes of the grid in a compact row-major order
+ * (axis a: 8 U_a positions k = v U_a + u, or all N_a when kept_u[a] == 0).
+ * ndim == 0 is the identity (every node, natural order). */
+#define PDB_MAP_MAX_DIMS 8
+typedef struct pdb_node_map {
+  int32_t ndim;                          /* grid rank, <= PDB_MAP_MAX_DIMS; 0 = identity */
+  int32_t kept_u[PDB_MAP_MAX_DIMS];      /* U_a (2 <= 8 U_a < N_a), or 0 = the whole axis */
+  int64_t dims[PDB_MAP_MAX_DIMS];        /* full grid shape (powers of two) */
+} pdb_node_map;
+
+/* Number of kept nodes (the compact grid size); <0 on an invalid map. */
+int64_t pdb_node_map_size(const pdb_node_map* map);
+
+/* pdb_det_batch_u32 / pdb_eval_det_fused_u32 over the kept nodes of `map`:
+ * node_lo / nodes are compact indices and out[i] = det at compact node
+ * node_lo + i.  The fused form's map covers the grid outer x n_last. */
+int32_t pdb_det_batch_map_u32(pdb_prime_ctx* ctx, const uint32_t* grids, int64_t grid_stride,
+                              const int32_t* entry_ids, int32_t r, const pdb_node_map* map,
+                              int64_t node_lo, int64_t nodes, uint32_t* out, void* scratch,
+                              size_t scratch_bytes, void* stream);
+int32_t pdb_eval_det_fused_map_u32(pdb_prime_ctx* ctx, const uint32_t* partial, int64_t outer,
+                                   int32_t ncoef, int32_t entries, int32_t n_last,
+                                   const int32_t* entry_ids, int32_t r, const pdb_node_map* map,
+                                   int64_t node_lo, int64_t nodes, uint32_t* out, void* scratch,
+                                   size_t scratch_bytes, void* stream);
+
+/* compact[pdb_node_map_size(map)] determinants at the kept nodes -> grid[prod dims]
+ * with every node's determinant (the same values det_grid computes there,
+ * determinant.py:92-133).  compact and grid must not overlap. */
+int32_t pdb_grid_expand_u32(pdb_prime_ctx* ctx, const uint32_t* compact, uint32_t* grid,
+                            const pdb_node_map* map, void* stream);
+
 /* Scalar condensation with the reference's pivot trail (determinant.py:57-84):
  * mat = r*r row-major residues (device); trail_vals[i]/trail_cols[i] = pivot of
  * step i (cols = -1 after an all-zero row); det_out[0] = det.  Scratch needs

@@ -120,6 +120,45 @@ int condense_run(PrimeCtx* ctx, const uint32_t* mat, int r, uint32_t* trail_vals
                  uint32_t* det_out, void* scratch, size_t scratch_bytes, cudaStream_t st);
 size_t crt_scratch_bytes(int P);
 int crt_limbs(int P);
+int grid_expand(PrimeCtx* ctx, const uint32_t* compact, uint32_t* grid, const NodeMap& map, const int64_t* dims,
+                cudaStream_t st);
+void expand_release(const PrimeCtx* ctx);
+
+// C-ABI node map -> device NodeMap (validated); false + error text when invalid.
+static bool make_node_map(const pdb_node_map* in, NodeMap* out, int64_t* size) {
+  *out = NodeMap{};
+  if (!in || in->ndim == 0) {
+    *size = -1;   // identity: caller's node count
+    return true;
+  }
+  if (in->ndim < 0 || in->ndim > PDB_MAP_DIMS) {
+    set_error("node map rank %d outside 1..%d", in->ndim, PDB_MAP_DIMS);
+    return false;
+  }
+  out->nd = in->ndim;
+  int64_t stride = 1, n = 1;
+  for (int a = in->ndim - 1; a >= 0; --a) {
+    const int64_t N = in->dims[a];
+    const int U = in->kept_u[a];
+    if (N < 1 || (N & (N - 1))) {
+      set_error("node map axis %d: %lld is not a power of two", a, (long long)N);
+      return false;
+    }
+    if (U != 0 && (N < 16 || U < 1 || 8ll * U >= N)) {
+      set_error("node map axis %d: kept u %d invalid for length %lld", a, U, (long long)N);
+      return false;
+    }
+    out->u[a] = U;
+    out->n8[a] = N / 8;
+    out->klen[a] = U ? 8ll * U : N;
+    out->stride[a] = stride;
+    stride *= N;
+    n *= out->klen[a];
+  }
+  *size = n;
+  return true;
+}
+
 int crt_mrc(const uint32_t* res, int P, int64_t n, int64_t res_stride, const uint32_t* primes_host,
             uint32_t* limbs, int L, uint8_t* neg, void* scratch, size_t scratch_bytes, int sms,
             cudaStream_t st);
@@ -235,6 +274,7 @@ int32_t pdb_prime_ctx_create_wide(uint64_t p, uint64_t omega, int32_t q, pdb_pri
 
 int32_t pdb_prime_ctx_destroy(pdb_prime_ctx* ctx) {
   if (!ctx) return 0;
+  expand_release(ctx);
   for (auto& T : ctx->tw)
     if (T.fwd) cudaFree(T.fwd);
   for (auto& T : ctx->tw64)
@@ -300,7 +340,70 @@ int32_t pdb_eval_det_fused_u32(pdb_prime_ctx* ctx, const uint32_t* partial, int6
   const Twiddles* T = ctx_twiddles(ctx, n_last);
   if (!T) return -2;
   FusedSrc src{partial, outer, ncoef, entries, n_last, T->full, T->full_s, ctx->m.p};
+  src.ulast = n_last / 8;
   return det_run(ctx, src, entry_ids, r, node_lo, nodes, out, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int64_t pdb_node_map_size(const pdb_node_map* map) {
+  NodeMap nm;
+  int64_t n = 0;
+  if (!map) { set_error("null node map"); return -2; }
+  if (!make_node_map(map, &nm, &n)) return -2;
+  if (n < 0) {
+    n = 1;
+    for (int a = 0; a < map->ndim; ++a) n *= map->dims[a];
+  }
+  return n;
+}
+
+int32_t pdb_det_batch_map_u32(pdb_prime_ctx* ctx, const uint32_t* grids, int64_t grid_stride,
+                              const int32_t* entry_ids, int32_t r, const pdb_node_map* map,
+                              int64_t node_lo, int64_t nodes, uint32_t* out, void* scratch,
+                              size_t scratch_bytes, void* stream) {
+  if (!narrow_ctx(ctx)) return -2;
+  StagedSrc src{grids, grid_stride};
+  int64_t n = 0;
+  if (!make_node_map(map, &src.map, &n)) return -2;
+  if (n >= 0 && (node_lo < 0 || node_lo + nodes > n)) { set_error("node range outside the node map"); return -2; }
+  return det_run(ctx, src, entry_ids, r, node_lo, nodes, out, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int32_t pdb_eval_det_fused_map_u32(pdb_prime_ctx* ctx, const uint32_t* partial, int64_t outer,
+                                   int32_t ncoef, int32_t entries, int32_t n_last,
+                                   const int32_t* entry_ids, int32_t r, const pdb_node_map* map,
+                                   int64_t node_lo, int64_t nodes, uint32_t* out, void* scratch,
+                                   size_t scratch_bytes, void* stream) {
+  if (!narrow_ctx(ctx)) return -2;
+  if (ncoef < 1 || entries < 1) { set_error("invalid fused arguments"); return -2; }
+  const Twiddles* T = ctx_twiddles(ctx, n_last);
+  if (!T) return -2;
+  FusedSrc src{partial, outer, ncoef, entries, n_last, T->full, T->full_s, ctx->m.p};
+  int64_t n = 0;
+  if (!make_node_map(map, &src.map, &n)) return -2;
+  src.ulast = n_last / 8;
+  if (n >= 0) {
+    int64_t full = 1;
+    for (int a = 0; a < map->ndim; ++a) full *= map->dims[a];
+    if (full != outer * n_last || map->dims[map->ndim - 1] != n_last) {
+      set_error("node map shape does not match outer x n_last");
+      return -2;
+    }
+    if (node_lo < 0 || node_lo + nodes > n) { set_error("node range outside the node map"); return -2; }
+    if (src.map.u[map->ndim - 1]) src.ulast = src.map.u[map->ndim - 1];
+  }
+  return det_run(ctx, src, entry_ids, r, node_lo, nodes, out, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int32_t pdb_grid_expand_u32(pdb_prime_ctx* ctx, const uint32_t* compact, uint32_t* grid,
+                            const pdb_node_map* map, void* stream) {
+  if (!narrow_ctx(ctx)) return -2;
+  NodeMap nm;
+  int64_t n = 0;
+  if (!map || map->ndim == 0) { set_error("grid_expand needs a pruned node map"); return -2; }
+  if (!make_node_map(map, &nm, &n)) return -2;
+  for (int a = 0; a < map->ndim; ++a)
+    if (map->kept_u[a] && !ctx_twiddles(ctx, (int)map->dims[a])) return -2;
+  return grid_expand(ctx, compact, grid, nm, map->dims, (cudaStream_t)stream);
 }
 
 int32_t pdb_condense_u32(pdb_prime_ctx* ctx, const uint32_t* mat, int32_t r, uint32_t* trail_vals,

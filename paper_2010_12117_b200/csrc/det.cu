@@ -66,8 +66,9 @@ det_robust(Src src, const int32_t* __restrict__ ids, int r, const int64_t* __res
   const int wpc = blockDim.x >> 5;
   const int64_t wstride = (int64_t)gridDim.x * wpc;
   for (int64_t idx = blockIdx.x * (int64_t)wpc + warp; idx < total; idx += wstride) {
-    const int64_t node = list ? list[idx] : node_lo + idx;
-    for (int e = lane; e < r * r; e += 32) A[e] = src.get(ids[e], node) % p;
+    const int64_t node = list ? list[idx] : node_lo + idx;   // compact index
+    const int64_t at = src.node(node);
+    for (int e = lane; e < r * r; e += 32) A[e] = src.at(ids[e], at) % p;
     __syncwarp();
     uint32_t pre = 1 % p, infl = 1 % p;
     uint64_t used0 = 0, used1 = 0;   // pivot columns so far (r <= 128)
@@ -142,11 +143,11 @@ det_small(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t n
 #pragma unroll
     for (int d = 0; d < D; ++d) {
       const int64_t idx = base + d * 32 + lane;
-      const int64_t node = node_lo + (idx < nodes ? idx : 0);
+      const int64_t node = src.node(node_lo + (idx < nodes ? idx : 0));
 #pragma unroll
       for (int i = 0; i < R; ++i)
 #pragma unroll
-        for (int j = 0; j < R; ++j) a[d][i][j] = src.get(ids[i * R + j], node);
+        for (int j = 0; j < R; ++j) a[d][i][j] = src.at(ids[i * R + j], node);
     }
     uint32_t pre[D], infl[D];
     bool ok[D];
@@ -339,8 +340,10 @@ static int launch_gj(PrimeCtx* ctx, int r, StagedSrc src, const int32_t* ids, in
 static int launch_gj(PrimeCtx* ctx, int r, FusedSrc src, const int32_t* ids, int64_t node_lo, int64_t nodes,
                      uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
   const GjGeom g = gj_pick(r, gj_lanes(r), true);
-  const bool dft8 = src.E <= 8 && src.NL >= 8 && src.NL % (8 * g.U) == 0 && node_lo % src.NL == 0 &&
-                    nodes % src.NL == 0;
+  // whole compact last-axis rows of 8 * ulast nodes, whole u-blocks per row
+  const int64_t klast = 8 * (int64_t)src.ulast;
+  const bool dft8 = src.E <= 8 && src.NL >= 8 && src.ulast >= 1 && src.ulast % g.U == 0 &&
+                    node_lo % klast == 0 && nodes % klast == 0;
   if (dft8) return launch_gj_mode<FusedSrc, true>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
   return launch_gj_mode<FusedSrc, false>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
 }

@@ -117,14 +117,32 @@ __device__ __forceinline__ int64_t gj_node_linear(int64_t it, int slot, const Gj
   return n < nodes ? n : -1;
 }
 
-__device__ __forceinline__ int64_t gj_node_dft8(int64_t it, int slot, const GjGeom& g, int NL) {
-  const int per_o = NL / (8 * g.U);
-  // per_o = NL / (8U) is a power of two whenever the DFT-8 fill is on (8U | NL, NL = 2^k)
-  const int lpo = __ffs(per_o) - 1;
-  const int64_t o = it >> lpo;
-  const int ublk = (int)(it & (per_o - 1));
+// DFT-8 fill geometry.  The launch covers whole compact last-axis rows of
+// 8 * ulast nodes (k = v * ulast + u, node u + (NL/8) v of the full axis; ulast
+// = NL/8 without pruning); iteration `it` takes the U consecutive u of u-block
+// ublk of compact outer row orel, i.e. full outer index o.
+struct GjD8 {
+  int64_t orel, o;
+  int ublk;
+};
+__device__ __forceinline__ GjD8 gj_d8(const FusedSrc& src, int U, int64_t it, int64_t node_lo) {
+  const int per_o = src.ulast / U;
+  const int64_t klast = 8 * (int64_t)src.ulast;
+  GjD8 d;
+  d.orel = it / per_o;
+  d.ublk = (int)(it - d.orel * per_o);
+  const int64_t oc = node_lo / klast + d.orel;   // compact outer row
+  d.o = src.map.nd ? src.map.full(oc * klast) / src.NL : oc;
+  return d;
+}
+
+// compact index (relative to the launch) of slot v * U + uu of iteration `it`
+__device__ __forceinline__ int64_t gj_node_dft8(const FusedSrc& src, int64_t it, int slot, const GjGeom& g) {
+  const int per_o = src.ulast / g.U;
+  const int64_t orel = it / per_o;
+  const int ublk = (int)(it - orel * per_o);
   const int v = slot / g.U, uu = slot - v * g.U;
-  return o * NL + ublk * g.U + uu + (int64_t)(NL / 8) * v;
+  return orel * 8 * (int64_t)src.ulast + (int64_t)v * src.ulast + ublk * g.U + uu;
 }
 
 // ---- fills: the RP x RP matrices of one iteration (padding = Montgomery identity) ----
@@ -134,7 +152,7 @@ __device__ __forceinline__ void gj_fill(const StagedSrc& src, uint32_t* mats, co
   const int slot = threadIdx.x % M;
   const int64_t n = gj_node_linear(it, slot, g, nodes);
   if (n >= 0) {
-    const uint32_t* col = src.grids + node_lo + n;
+    const uint32_t* col = src.grids + src.node(node_lo + n);
     uint32_t* dst = mats + (size_t)slot * g.MS;
     const int first = threadIdx.x / M, step = blockDim.x / M;
     if (dense) {
@@ -160,9 +178,10 @@ __device__ __forceinline__ void gj_fill(const FusedSrc& src, uint32_t* mats, con
   const int64_t n = gj_node_linear(it, slot, g, nodes);
   if (n < 0) return;
   uint32_t* dst = mats + (size_t)slot * g.MS;
+  const int64_t at = src.node(node_lo + n);
   GjPos pi(threadIdx.x / M, blockDim.x / M, RP);
   for (; pi.i < RP; pi.next())
-    dst[pi.i * S + pi.j] = (pi.i < r && pi.j < r) ? src.get(__ldg(ids + pi.i * r + pi.j), node_lo + n)
+    dst[pi.i * S + pi.j] = (pi.i < r && pi.j < r) ? src.at(__ldg(ids + pi.i * r + pi.j), at)
                                                   : (pi.i == pi.j ? one : 0u);
 }
 
@@ -175,10 +194,9 @@ __device__ __forceinline__ void gj_fill_dft8_e(const FusedSrc& src, uint32_t* ma
                                                const int32_t* ids, int64_t it, int64_t node_lo, uint32_t one) {
   const int r = g.r, RP = g.RP, S = g.S, U = g.U, NL = src.NL, k = src.k;
   const uint32_t p = src.p;
-  const int per_o = NL / (8 * U);
-  const int lpo = __ffs(per_o) - 1;   // per_o and NL are powers of two on this path
-  const int64_t o = (node_lo >> (__ffs(NL) - 1)) + (it >> lpo);
-  const int ublk = (int)(it & (per_o - 1));
+  const GjD8 d8 = gj_d8(src, U, it, node_lo);
+  const int64_t o = d8.o;
+  const int ublk = d8.ublk;
   const int step8 = NL / 8;
   uint32_t w[4], ws[4];
 #pragma unroll
@@ -250,10 +268,9 @@ __device__ __forceinline__ void gj_fill_dft8_dense(const FusedSrc& src, uint32_t
   const int U = UC ? UC : g.U, NL = src.NL, k = src.k, n = NC ? NC : g.r * g.r;
   const int MS = MSC ? MSC : g.MS;
   const uint32_t p = src.p;
-  const int per_o = NL / (8 * U);
-  const int lpo = __ffs(per_o) - 1;   // per_o and NL are powers of two on this path
-  const int64_t o = (node_lo >> (__ffs(NL) - 1)) + (it >> lpo);
-  const int ublk = (int)(it & (per_o - 1));
+  const GjD8 d8 = gj_d8(src, U, it, node_lo);
+  const int64_t o = d8.o;
+  const int ublk = d8.ublk;
   const int step8 = NL / 8;
   uint32_t w[4], ws[4];
 #pragma unroll
@@ -609,7 +626,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
     else gj_fill(src, mats, g, ids, it, node_lo, nodes, one, dense);
     __syncthreads();
     int64_t node;
-    if constexpr (DFT8) node = gj_node_dft8(it, slot, g, src.NL);
+    if constexpr (DFT8) node = gj_node_dft8(src, it, slot, g);
     else node = gj_node_linear(it, slot, g, nodes);
     if (node < 0) continue;
 

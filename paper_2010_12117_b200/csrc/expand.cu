@@ -1,0 +1,234 @@
+// Determinants at the pruned node set -> the full evaluation grid.
+//
+// The reference evaluates det(M) at every node of the grid (pipeline.py:374-392)
+// and interpolates with a full inverse NTT.  The determinant has degree <= D_a
+// in variable a (pipeline.py:184-196), and on an axis of N nodes
+//     f(x) = sum_{l<8} x^l g_l(x^8),   deg g_l <= floor(D_a / 8) < U,
+// so the values of f at the nodes u + (N/8) v with u < U (v < 8) fix every g_l
+// at the first U of the N/8 points y_u = w^(8u) -- hence f at every node.
+// Per line, with z_l(u) = (1/8) sum_v f(w^(u + N/8 v)) w8^(-lv) = w^(ul) g_l(y_u):
+//     y_l(u') = sum_{u<U} w^(l(u'-u)) L_u(y_u') z_l(u),   u' = U .. N/8-1
+//     f(w^(u' + N/8 v)) = sum_l y_l(u') w8^(lv),
+// L_u the Lagrange basis on y_0..y_{U-1}.  The extended values are exactly
+// the determinants the reference computes at those nodes (the polynomial
+// identity holds mod p), so the grid -- and every artifact built from it --
+// is bit-identical; only ~prod_a 8 U_a / N_a of the determinants are computed
+// (C5: 176^3 of 256^3 = 33 %).
+//
+// grid_expand: scatter the compact determinants into the grid, then extend
+// along each pruned axis from the last to the first; the lines of axis a run
+// over the kept nodes of the axes before it and every node of the axes after.
+#include <map>
+#include <vector>
+
+#include "pdb_internal.cuh"
+
+namespace pdb {
+
+struct ExpandTables {
+  int N = 0, U = 0;
+  uint32_t* dev = nullptr;   // [64] iDFT-8 (incl. 1/8), [64] DFT-8, [8][N/8-U][U] extension; Montgomery forms
+};
+
+static std::mutex g_xlock;
+static std::map<std::tuple<const PrimeCtx*, int, int>, ExpandTables> g_tables;
+
+static uint64_t mulm(uint64_t a, uint64_t b, uint64_t p) { return (uint64_t)((unsigned __int128)a * b % p); }
+static uint64_t powm(uint64_t a, uint64_t e, uint64_t p) {
+  uint64_t r = 1 % p;
+  a %= p;
+  for (; e; e >>= 1, a = mulm(a, a, p))
+    if (e & 1) r = mulm(r, a, p);
+  return r;
+}
+
+static const ExpandTables* expand_tables(PrimeCtx* ctx, int N, int U) {
+  std::lock_guard<std::mutex> guard(g_xlock);
+  auto key = std::make_tuple((const PrimeCtx*)ctx, N, U);
+  auto it = g_tables.find(key);
+  if (it != g_tables.end()) return &it->second;
+  const uint64_t p = ctx->p;
+  const int l = 31 - __builtin_clz((unsigned)N);
+  const uint64_t w = powm(ctx->omega, 1ull << (ctx->q - l), p);   // w_N
+  const uint64_t w8 = powm(w, N / 8, p), w8i = powm(w8, p - 2, p);
+  const uint64_t inv8 = powm(8, p - 2, p);
+  const uint64_t R = ((uint64_t)1 << 32) % p;
+  const int N8 = N / 8, T = N8 - U;
+  std::vector<uint32_t> h(128 + (size_t)8 * T * U);
+  for (int a = 0; a < 8; ++a)
+    for (int b = 0; b < 8; ++b) {
+      h[a * 8 + b] = (uint32_t)mulm(mulm(powm(w8i, (uint64_t)a * b, p), inv8, p), R, p);   // [l][v]
+      h[64 + a * 8 + b] = (uint32_t)mulm(powm(w8, (uint64_t)a * b, p), R, p);             // [v][l]
+    }
+  // Lagrange basis on y_u = w^(8u), u < U, evaluated at y_u', u' = U..N8-1
+  std::vector<uint64_t> y(N8), bw(U);
+  for (int j = 0; j < N8; ++j) y[j] = powm(w, 8ull * j, p);
+  for (int u = 0; u < U; ++u) {
+    uint64_t d = 1;
+    for (int j = 0; j < U; ++j)
+      if (j != u) d = mulm(d, (y[u] + p - y[j]) % p, p);
+    bw[u] = powm(d, p - 2, p);   // barycentric weight
+  }
+  for (int t = 0; t < T; ++t) {
+    const uint64_t yt = y[U + t];
+    uint64_t ell = 1;
+    for (int j = 0; j < U; ++j) ell = mulm(ell, (yt + p - y[j]) % p, p);
+    for (int u = 0; u < U; ++u) {
+      const uint64_t Lu = mulm(mulm(ell, bw[u], p), powm((yt + p - y[u]) % p, p - 2, p), p);
+      for (int ll = 0; ll < 8; ++ll) {
+        const uint64_t tw = powm(w, (uint64_t)ll * (uint64_t)(U + t - u), p);
+        h[128 + ((size_t)ll * T + t) * U + u] = (uint32_t)mulm(mulm(tw, Lu, p), R, p);
+      }
+    }
+  }
+  ExpandTables X;
+  X.N = N;
+  X.U = U;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaMalloc(&X.dev, h.size() * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemcpy(X.dev, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    set_error("expand table allocation: %s", cudaGetErrorString(e));
+    return nullptr;
+  }
+  return &(g_tables[key] = X);
+}
+
+void expand_release(const PrimeCtx* ctx) {
+  std::lock_guard<std::mutex> guard(g_xlock);
+  for (auto it = g_tables.begin(); it != g_tables.end();) {
+    if (std::get<0>(it->first) == ctx) {
+      cudaFree(it->second.dev);
+      it = g_tables.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+// sum_i a[i] * bR[i] mod p (bR Montgomery forms), canonical; up to 8 products per
+// reduction for p < 2^30, 2 otherwise
+__device__ __forceinline__ uint32_t dot_mont(const uint32_t* a, int sa, const uint32_t* bR, int n, const Mod32& m) {
+  const int cap = m.fast() ? 8 : 2;
+  uint32_t s = 0;
+  for (int i0 = 0; i0 < n; i0 += cap) {
+    uint64_t acc = 0;
+    const int i1 = i0 + cap < n ? i0 + cap : n;
+    for (int i = i0; i < i1; ++i) acc = mad_wide(a[(size_t)i * sa], __ldg(bR + i), acc);
+    s = add_mod(s, canon32(redc(acc, m), m), m.p);
+  }
+  return s;
+}
+
+__global__ void grid_scatter(const uint32_t* __restrict__ compact, uint32_t* __restrict__ grid, int64_t n,
+                             NodeMap map) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    grid[map.full(c)] = compact[c];
+}
+
+// One CTA per tile of TI columns; column j = (line j / inner, position j % inner);
+// a line's element n sits at outer(line) + n * inner + j % inner.
+__global__ void __launch_bounds__(256)
+grid_extend(uint32_t* __restrict__ grid, NodeMap outer_map, int64_t lines, int64_t inner, int N, int U, int TI,
+            const uint32_t* __restrict__ tab, Mod32 m) {
+  extern __shared__ uint32_t xs[];
+  const int N8 = N / 8, T = N8 - U, K = 8 * U;
+  uint32_t* kept = xs;                  // [K][TI]   kept values, row k = v U + u
+  uint32_t* zs = kept + K * TI;         // [8][U][TI]
+  __shared__ int64_t cbase[32];
+  const int64_t cols = lines * inner;
+  const int64_t tiles = (cols + TI - 1) / TI;
+  const bool rowfast = inner < TI;      // coalesce along the line when lines are short-strided
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t j0 = tile * TI;
+    __syncthreads();
+    if (threadIdx.x < TI) {
+      const int64_t j = j0 + threadIdx.x;
+      cbase[threadIdx.x] = j < cols ? outer_map.full(j / inner) * N * inner + j % inner : -1;
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < K * TI; w += blockDim.x) {
+      const int k = rowfast ? w % K : w / TI, t = rowfast ? w / K : w % TI;
+      const int u = k % U, v = k / U;
+      const int64_t b = cbase[t];
+      kept[k * TI + t] = b >= 0 ? grid[b + (int64_t)(u + N8 * v) * inner] : 0u;
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < 8 * U * TI; w += blockDim.x) {   // z_l(u) = iDFT8
+      const int t = w % TI, lu = w / TI, l = lu / U, u = lu % U;
+      zs[(l * U + u) * TI + t] = dot_mont(kept + u * TI + t, U * TI, tab + l * 8, 8, m);
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < T * TI; w += blockDim.x) {
+      const int t = rowfast ? w / T : w % TI, tt = rowfast ? w % T : w / TI;
+      const int64_t b = cbase[t];
+      if (b < 0) continue;
+      uint32_t yl[8];
+#pragma unroll
+      for (int l = 0; l < 8; ++l) yl[l] = dot_mont(zs + (l * U) * TI + t, TI, tab + 128 + ((size_t)l * T + tt) * U, U, m);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        // 8 products: one reduction for p < 2^30, pairs otherwise
+        const uint32_t* f = tab + 64 + v * 8;
+        uint32_t s = 0;
+#pragma unroll
+        for (int h = 0; h < 8; h += 2) {
+          uint64_t acc = mad_wide(yl[h], __ldg(f + h), mad_wide(yl[h + 1], __ldg(f + h + 1), 0ull));
+          if (m.fast()) {
+#pragma unroll
+            for (int q = h + 2; q < 8; ++q) acc = mad_wide(yl[q], __ldg(f + q), acc);
+            s = canon32(redc(acc, m), m);
+            break;
+          }
+          s = add_mod(s, canon32(redc(acc, m), m), m.p);
+        }
+        grid[b + (int64_t)(U + tt + N8 * v) * inner] = s;
+      }
+    }
+  }
+}
+
+int grid_expand(PrimeCtx* ctx, const uint32_t* compact, uint32_t* grid, const NodeMap& map, const int64_t* dims,
+                cudaStream_t st) {
+  int64_t n = 1;
+  for (int a = 0; a < map.nd; ++a) n *= map.klen[a];
+  if (map.nd == 0) {
+    set_error("grid_expand needs a pruned node map");
+    return -2;
+  }
+  {
+    const int64_t blocks = (n + 255) / 256;
+    const int g = (int)(blocks < (int64_t)ctx->sms * 16 ? blocks : (int64_t)ctx->sms * 16);
+    grid_scatter<<<g, 256, 0, st>>>(compact, grid, n, map);
+    count_launch();
+    if (int rc = check_launch("grid_scatter")) return rc;
+  }
+  for (int a = map.nd - 1; a >= 0; --a) {
+    if (!map.u[a]) continue;
+    const int N = (int)dims[a], U = map.u[a];
+    const ExpandTables* X = expand_tables(ctx, N, U);
+    if (!X) return -1;
+    NodeMap om = map;            // the axes before a: kept nodes only
+    om.nd = a;
+    int64_t lines = 1, inner = 1;
+    for (int b = 0; b < a; ++b) lines *= map.klen[b];
+    for (int b = a + 1; b < map.nd; ++b) inner *= dims[b];
+    // om.full(line): the line's row-major index over dims[0..a) (units of N * inner words)
+    for (int b = 0; b < a; ++b) om.stride[b] = map.stride[b] / ((int64_t)N * inner);
+    int TI = 32;
+    while (TI > 1 && (size_t)(8 * U + 8 * U) * TI * 4 > 96 * 1024) TI >>= 1;
+    const size_t smem = (size_t)(8 * U + 8 * U) * TI * sizeof(uint32_t);
+    const int64_t tiles = (lines * inner + TI - 1) / TI;
+    const int g = (int)(tiles < (int64_t)ctx->sms * 8 ? tiles : (int64_t)ctx->sms * 8);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(grid_extend, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    grid_extend<<<g, 256, smem, st>>>(grid, om, lines, inner, N, U, TI, X->dev, ctx->m);
+    count_launch();
+    if (int rc = check_launch("grid_extend")) return rc;
+  }
+  return 0;
+}
+
+}  // namespace pdb

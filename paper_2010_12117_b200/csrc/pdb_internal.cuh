@@ -85,12 +85,57 @@ void count_launch(long long n = 1);
 int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t* dims,
              const int64_t* ext, int axis, bool inverse, cudaStream_t st);
 
+// ---- pruned node sets ----------------------------------------------------------
+// The determinant is a polynomial of degree <= D_a in variable a (the plan's
+// degree bound), so on an axis of N >= 16 nodes only the nodes
+//     {u + (N/8) v : u < U, v < 8},   U >= floor(D_a / 8) + 1,
+// need a determinant: writing f(x) = sum_{l<8} x^l g_l(x^8), every g_l has
+// degree <= floor(D_a/8) < U, so its values at the first U of the N/8 points
+// (w^8)^u determine the rest (expand.cu).  A NodeMap enumerates the kept nodes
+// of a grid in a compact row-major order: axis a has klen[a] = 8 U_a compact
+// positions k = v U_a + u (or all N_a when u[a] == 0), and full() returns the
+// node's position in the full row-major grid.  nd == 0 is the identity.
+#define PDB_MAP_DIMS 8
+struct NodeMap {
+  int32_t nd = 0;
+  int32_t u[PDB_MAP_DIMS] = {};          // kept u per axis, 0 = whole axis
+  int64_t klen[PDB_MAP_DIMS] = {};       // compact extent per axis
+  int64_t n8[PDB_MAP_DIMS] = {};         // N_a / 8
+  int64_t stride[PDB_MAP_DIMS] = {};     // row-major stride of axis a in the full grid
+  __host__ __device__ __forceinline__ int64_t full(int64_t c) const {
+    if (nd == 0) return c;
+    int64_t off = 0;
+    if (c < (1ll << 32)) {   // 32-bit div/mod on the common path
+      uint32_t cc = (uint32_t)c;
+      for (int a = nd - 1; a >= 0; --a) {
+        const uint32_t kl = (uint32_t)klen[a];
+        const uint32_t k = cc % kl;
+        cc /= kl;
+        const int64_t ax = u[a] ? (int64_t)(k % (uint32_t)u[a]) + n8[a] * (k / (uint32_t)u[a]) : (int64_t)k;
+        off += ax * stride[a];
+      }
+      return off;
+    }
+    for (int a = nd - 1; a >= 0; --a) {
+      const int64_t k = c % klen[a];
+      c /= klen[a];
+      const int64_t ax = u[a] ? k % u[a] + n8[a] * (k / u[a]) : k;
+      off += ax * stride[a];
+    }
+    return off;
+  }
+};
+
 // ---- entry sources for the determinant kernels ---------------------------------
+// Kernels index nodes in the compact space of `map` (identity: the grid);
+// node(c) is the full-grid node, at(e, node) the value of entry e there.
 // Staged: materialised entry grids [k][stride] (node-major within an entry).
 struct StagedSrc {
   const uint32_t* grids;
   int64_t stride;
-  __device__ __forceinline__ uint32_t get(int e, int64_t node) const {
+  NodeMap map;
+  __device__ __forceinline__ int64_t node(int64_t c) const { return map.full(c); }
+  __device__ __forceinline__ uint32_t at(int e, int64_t node) const {
     return __ldg(grids + (int64_t)e * stride + node);
   }
 };
@@ -109,7 +154,10 @@ struct FusedSrc {
   const uint32_t* xs;    // w^c, c < NL
   const uint32_t* xss;   // companions
   uint32_t p;
-  __device__ __forceinline__ uint32_t get(int e, int64_t node) const {
+  NodeMap map;
+  int ulast = 0;         // kept u of the last axis (NL / 8 when it is not pruned)
+  __device__ __forceinline__ int64_t node(int64_t c) const { return map.full(c); }
+  __device__ __forceinline__ uint32_t at(int e, int64_t node) const {
     int64_t o = node / NL;
     int c = (int)(node - o * NL);
     const uint32_t* a = part + o * E * (int64_t)k + e;

@@ -23,6 +23,10 @@ Two FFT/DET modes, same results:
 
 Unit names, notification order, skip-if-stored and the workspace header
 logic follow the reference exactly, so kill/resume behaves identically.
+Without a workspace, fused mode reports the reference's fine-grained units
+too (p{i}/fft/e{j}, p{i}/det, p{i}/ifft, crt); with one, it reports and
+persists the p{i}/ifft units only, because it never materialises the entry
+grids or the determinant grid that the finer units name.
 Stage timings are CUDA-event seconds of each stage's device work.
 """
 
@@ -38,7 +42,7 @@ from .checkpoint import Workspace, digest_of
 from .crt import device_lift, wide_primes
 from .errors import StaleWorkspaceError
 from .layout import CoeffTensor, PolyMatrix, residue_dtype
-from .planner import Plan, PipelineConfig, StageTimings, plan
+from .planner import Plan, PipelineConfig, StageTimings, degree_bound, plan
 
 INPUT_FILE = "input.json"
 PLAN_FILE = "plan.json"
@@ -130,6 +134,12 @@ class DevicePlan:
         self.wide = wide_primes([s.p for s in pl.primes])
         self.word = native.word_dtype(self.wide)
         self.staged = staged or self.vn == 0 or self.wide
+        for t in m.unique_entries:
+            # the reference pads every entry to the plan shape (pipeline.py:361) and
+            # pad_to refuses to shrink (tensor.py:219-220); a larger entry box would
+            # otherwise walk into the neighbouring entry's lines
+            if len(t.shape) != self.vn or any(a > b for a, b in zip(t.shape, self.shape)):
+                raise ValueError("cannot shrink %s to %s" % (tuple(t.shape), self.shape))
         if not self.staged:
             self.E = max(t.shape[-1] for t in m.unique_entries)
             self.outer = self.nodes // self.shape[-1]
@@ -138,6 +148,9 @@ class DevicePlan:
             prep = _python_terms(m, self.shape, self.nodes, self.staged, self.E if not self.staged else 0)
         mag, neg, L, pos = prep
         self.count = len(neg)
+        # coefficients are entry-major: entry e owns [entry_starts[e], entry_starts[e+1])
+        owner = pos // self.nodes if self.staged else pos % self.k
+        self.entry_starts = np.searchsorted(owner, np.arange(self.k + 1)).tolist()
         self.L = L
         self.mag = torch.from_numpy(mag.view(np.int32).copy()).to(device) if self.count else \
             torch.zeros(1, dtype=torch.int32, device=device)
@@ -148,9 +161,35 @@ class DevicePlan:
         self.ids = torch.tensor(list(m.entry_ids), dtype=torch.int32, device=device)
         # per-axis coefficient extents (for NTT pruning): largest exponent + 1
         self.ext = [max(t.shape[a] for t in m.unique_entries) for a in range(self.vn)]
+        # pruned node set (csrc/expand.cu): determinants only where the degree
+        # bound needs them, the rest of the grid is extended exactly
+        self.kept_u = kept_u(self.shape, degree_bound(m), even_last=not self.staged) \
+            if PRUNE and not self.wide else [0] * self.vn
+        self.nmap = native.node_map(self.shape, self.kept_u) if self.vn else None
+        self.sel = native.node_map_size(self.nmap) if self.nmap is not None else self.nodes
+        self.klen = [8 * u if u else n for n, u in zip(self.shape, self.kept_u)]
 
     def buffer_words(self) -> int:
         return self.k * self.nodes if self.staged else self.k * self.outer * self.E
+
+
+#: determinants only at the kept nodes of the degree bound (False: every node, as the reference)
+PRUNE = os.environ.get("PDB_NO_PRUNE", "") == ""
+
+
+def kept_u(shape, degrees, even_last: bool = False) -> list:
+    """Per axis, the u-count U of the kept nodes {u + (N/8) v : u < U, v < 8}
+    (0 = every node): det(M) has degree <= D_a in variable a, so
+    U = floor(D_a / 8) + 1 suffices.  even_last rounds the last axis's U up to
+    even (the fused kernel evaluates pairs of u per iteration).  Axes shorter
+    than 16 or with 8 U >= N keep every node."""
+    out = []
+    for a, (n, d) in enumerate(zip(shape, degrees)):
+        u = min(int(d), n - 1) // 8 + 1
+        if even_last and a == len(shape) - 1:
+            u += u & 1
+        out.append(u if n >= 16 and 8 * u < n else 0)
+    return out
 
 
 def _python_terms(m: PolyMatrix, shape, nodes, staged, E):
@@ -222,7 +261,15 @@ def choose_staged(m: PolyMatrix, pl: Plan, ws) -> bool:
         return True
     if FORCE_MODE is not None and ws is None:
         return FORCE_MODE == "staged"
-    grid_bytes = 4 * m.k * pl.node_count
+    wide = wide_primes([s.p for s in pl.primes])
+    grid_bytes = (8 if wide else 4) * m.k * pl.node_count
+    if wide:
+        # the u64 path has no fused kernel: it is staged or nothing
+        if grid_bytes > STAGED_LIMIT:
+            raise ValueError("wide-prime plan needs %.1f GB of staged u64 grids (limit %.1f GB, "
+                             "PDB_STAGED_LIMIT); primes >= 2^31 have no fused path"
+                             % (grid_bytes / 1e9, STAGED_LIMIT / 1e9))
+        return True
     if ws is not None and grid_bytes <= STAGED_LIMIT:
         return True
     return grid_bytes <= STAGED_LIMIT and pl.r <= 8 or grid_bytes <= STAGED_LIMIT // 4
@@ -268,8 +315,8 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
     mine = shard.my_primes(whole, rank, size)
     residues = torch.empty((len(mine), nodes), dtype=dp.word, device=device)
     work = torch.empty(dp.buffer_words() or 1, dtype=dp.word, device=device)
-    det_chunk = nodes if dp.staged else min(nodes, FUSED_CHUNK)
-    det_buf = torch.empty(nodes, dtype=dp.word, device=device)
+    det_chunk = det_chunk_size(dp)
+    det_buf = torch.empty(dp.sel, dtype=dp.word, device=device)
     scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, det_chunk, dp.wide), device)
     events = []
     for row, pi in enumerate(mine):
@@ -282,9 +329,8 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
         t0 = _Timer(torch, stream).mark()
         _fft_stage(dp, ctx, work, ws, pi, cfg)
         t1 = _Timer(torch, stream).mark()
-        _det_stage(dp, ctx, work, det_buf, scratch, det_chunk, ws, pi, cfg)
+        _det_stage(dp, ctx, work, det_buf, scratch, det_chunk, ws, pi, cfg, residues[row])
         t2 = _Timer(torch, stream).mark()
-        residues[row].copy_(det_buf)
         native.ntt_multi(ctx, residues[row], 1, dp.shape, None, range(dp.vn), True)
         t3 = _Timer(torch, stream).mark()
         events.append((t0, t1, t2, t3))
@@ -318,9 +364,9 @@ def _slab_primes(dp: DevicePlan, primes, work, det_buf, scratch, chunk, rank, si
     the determinants of its slab of the slowest axis, all-gathers the slabs and
     runs the inverse NTT of the full grid."""
     pl = dp.pl
-    n0 = dp.shape[0]
-    inner = dp.nodes // n0
-    lo, hi = shard.my_slab(n0, rank, size)
+    k0 = dp.klen[0]           # slabs of the kept nodes' slowest axis
+    inner = dp.sel // k0
+    lo, hi = shard.my_slab(k0, rank, size)
     rows = torch.empty((len(primes), dp.nodes), dtype=dp.word, device=det_buf.device)
     for j, pi in enumerate(primes):
         ctx = native.prime_context(pl.primes[pi], det_buf.device.index, dp.wide)
@@ -328,9 +374,9 @@ def _slab_primes(dp: DevicePlan, primes, work, det_buf, scratch, chunk, rank, si
         _fft_stage(dp, ctx, work, None, pi, cfg)
         t1 = _Timer(torch, stream).mark()
         _det_range(dp, ctx, work, det_buf, scratch, chunk, lo * inner, (hi - lo) * inner)
-        full = shard.gather_slabs(det_buf[lo * inner: hi * inner], n0, inner, rank, size)
+        full = shard.gather_slabs(det_buf[lo * inner: hi * inner], k0, inner, rank, size)
+        _expand(dp, ctx, full, rows[j])
         t2 = _Timer(torch, stream).mark()
-        rows[j].copy_(full)
         native.ntt_multi(ctx, rows[j], 1, dp.shape, None, range(dp.vn), True)
         t3 = _Timer(torch, stream).mark()
         events.append((t0, t1, t2, t3))
@@ -338,19 +384,45 @@ def _slab_primes(dp: DevicePlan, primes, work, det_buf, scratch, chunk, rank, si
     return rows
 
 
+def det_chunk_size(dp: DevicePlan) -> int:
+    """Nodes per determinant launch: all of them staged; in fused mode chunks of
+    ~FUSED_CHUNK made of whole kept last-axis rows (the DFT-8 fill's unit)."""
+    if dp.staged:
+        return max(dp.sel, 1)
+    row = dp.klen[-1]
+    return max(row, min(dp.sel, FUSED_CHUNK) // row * row)
+
+
 def _det_range(dp: DevicePlan, ctx, work, det_buf, scratch, chunk, node_lo: int, count: int):
-    """Determinants of nodes [node_lo, node_lo + count) into det_buf (same positions)."""
+    """Determinants of the kept nodes [node_lo, node_lo + count) (compact order of
+    dp.nmap; every node in natural order without pruning) into det_buf."""
     pl = dp.pl
     if count == 0:
         return
     if dp.staged:
-        native.det_batch(ctx, work, dp.nodes, dp.ids, pl.r, node_lo, count, det_buf[node_lo:node_lo + count], scratch)
+        out = det_buf[node_lo:node_lo + count]
+        if dp.nmap is None:
+            native.det_batch(ctx, work, dp.nodes, dp.ids, pl.r, node_lo, count, out, scratch)
+        else:
+            native.det_batch_map(ctx, work, dp.nodes, dp.ids, pl.r, dp.nmap, node_lo, count, out, scratch)
         return
     n_last = dp.shape[-1]
     for lo in range(node_lo, node_lo + count, chunk):
         cnt = min(chunk, node_lo + count - lo)
-        native.eval_det_fused(ctx, work, dp.outer, dp.E, dp.k, n_last, dp.ids, pl.r, lo, cnt,
-                              det_buf[lo:lo + cnt], scratch)
+        if dp.nmap is None:
+            native.eval_det_fused(ctx, work, dp.outer, dp.E, dp.k, n_last, dp.ids, pl.r, lo, cnt,
+                                  det_buf[lo:lo + cnt], scratch)
+        else:
+            native.eval_det_fused_map(ctx, work, dp.outer, dp.E, dp.k, n_last, dp.ids, pl.r, dp.nmap, lo, cnt,
+                                      det_buf[lo:lo + cnt], scratch)
+
+
+def _expand(dp: DevicePlan, ctx, compact, grid):
+    """Determinants at the kept nodes -> the full determinant grid (csrc/expand.cu)."""
+    if dp.nmap is None:
+        grid.copy_(compact[:dp.nodes])
+    else:
+        native.grid_expand(ctx, compact, grid, dp.nmap)
 
 
 def _sparse_leading_axes(dp: DevicePlan) -> bool:
@@ -376,8 +448,12 @@ def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
             work.zero_()
         native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, work)
         native.ntt_multi(ctx, work, 1, dims, ext, range(dp.vn - 1), False)
+        if ws is None:
+            # progress only: fused mode stores no fft/det artifacts, so with a
+            # workspace it reports (and checkpoints) p{i}/ifft units alone
+            for eid in range(dp.k):
+                cfg._notify("p%d/fft/e%d" % (pi, eid))
         return
-    work.zero_()
     todo = []
     for eid in range(dp.k):
         unit = "p%d/fft/e%d" % (pi, eid)
@@ -389,15 +465,17 @@ def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
     if not todo:
         return
     if len(todo) < dp.k:
-        # keep stored grids: scatter into a side buffer and transform only the todo entries
-        native._torch()
-        fresh = work.new_zeros(dp.k * dp.nodes)
-        native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, fresh)
+        # keep the stored grids: scatter and transform only the todo entries, in
+        # place (each entry's coefficients are one contiguous run of the upload)
         for eid in todo:
-            sl = fresh[eid * dp.nodes:(eid + 1) * dp.nodes]
+            sl = work[eid * dp.nodes:(eid + 1) * dp.nodes]
+            sl.zero_()
+            lo, hi = dp.entry_starts[eid], dp.entry_starts[eid + 1]
+            if hi > lo:
+                native.reduce_scatter(ctx, dp.mag[lo:], dp.neg[lo:], dp.pos[lo:], hi - lo, dp.L, work)
             native.ntt_multi(ctx, sl, 1, dp.shape, dp.ext, range(dp.vn), False)
-            work[eid * dp.nodes:(eid + 1) * dp.nodes].copy_(sl)
     else:
+        work.zero_()
         native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, work)
         native.ntt_multi(ctx, work, dp.k, dp.shape, dp.ext, range(dp.vn), False)
     for eid in todo:
@@ -408,16 +486,23 @@ def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
         cfg._notify(unit)
 
 
-def _det_stage(dp: DevicePlan, ctx, work, det_buf, scratch, chunk, ws, pi, cfg):
+def _det_stage(dp: DevicePlan, ctx, work, det_buf, scratch, chunk, ws, pi, cfg, out):
+    """The full determinant grid of one prime into `out` ([nodes])."""
     pl = dp.pl
     unit = "p%d/det" % pi
     if ws is not None and ws.has(unit):
-        det_buf.copy_(native.to_device_words(_load_grid(ws, unit, pl), dp.wide))
+        out.copy_(native.to_device_words(_load_grid(ws, unit, pl), dp.wide))
         return
-    _det_range(dp, ctx, work, det_buf, scratch, chunk, 0, dp.nodes)
-    if dp.staged:   # fused mode has no det (or fft) units: it checkpoints per prime
+    if dp.nmap is None:
+        _det_range(dp, ctx, work, out, scratch, chunk, 0, dp.nodes)
+    else:
+        _det_range(dp, ctx, work, det_buf, scratch, chunk, 0, dp.sel)
+        _expand(dp, ctx, det_buf, out)
+    if dp.staged:
         if ws is not None:
-            ws.store_residues(unit, native.to_host_words(det_buf, dp.wide), pl.shape)
+            ws.store_residues(unit, native.to_host_words(out, dp.wide), pl.shape)
+        cfg._notify(unit)
+    elif ws is None:   # fused mode: progress only (no det artifact; see _fft_stage)
         cfg._notify(unit)
 
 
@@ -456,8 +541,9 @@ class PrimeStages:
         self.dp = DevicePlan(m, pl, self.device, staged)
         dp = self.dp
         self.work = torch.empty(dp.buffer_words() or 1, dtype=dp.word, device=self.device)
-        self.chunk = dp.nodes if dp.staged else min(dp.nodes, FUSED_CHUNK)
+        self.chunk = det_chunk_size(dp)
         self.det = torch.empty(dp.nodes, dtype=dp.word, device=self.device)
+        self.compact = torch.empty(dp.sel, dtype=dp.word, device=self.device)
         self.scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, self.chunk, dp.wide), self.device)
         self._cfg = PipelineConfig()
 
@@ -468,7 +554,8 @@ class PrimeStages:
         _fft_stage(self.dp, self.ctx(pi), self.work, None, pi, self._cfg)
 
     def determinants(self, pi):
-        _det_stage(self.dp, self.ctx(pi), self.work, self.det, self.scratch, self.chunk, None, pi, self._cfg)
+        _det_stage(self.dp, self.ctx(pi), self.work, self.compact, self.scratch, self.chunk, None, pi, self._cfg,
+                   self.det)
 
     def interpolate(self, pi):
         native.ntt_multi(self.ctx(pi), self.det, 1, self.dp.shape, None, range(self.dp.vn), True)

@@ -33,6 +33,17 @@ _lock = threading.Lock()
 _c_i32, _c_i64, _c_u32, _c_u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
 _c_size, _c_vp = ctypes.c_size_t, ctypes.c_void_p
 
+MAP_MAX_DIMS = 8
+
+
+class NodeMapC(ctypes.Structure):
+    """pdb_node_map (include/polydet_b200.h): the kept nodes of a pruned grid."""
+    _fields_ = [("ndim", ctypes.c_int32), ("kept_u", ctypes.c_int32 * MAP_MAX_DIMS),
+                ("dims", ctypes.c_int64 * MAP_MAX_DIMS)]
+
+
+_c_map = ctypes.POINTER(NodeMapC)
+
 _SIGNATURES = {
     "pdb_last_error": (ctypes.c_char_p, []),
     "pdb_version": (_c_i32, []),
@@ -48,6 +59,12 @@ _SIGNATURES = {
                                    _c_vp, _c_size, _c_vp]),
     "pdb_eval_det_fused_u32": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_vp, _c_i32, _c_i64,
                                         _c_i64, _c_vp, _c_vp, _c_size, _c_vp]),
+    "pdb_node_map_size": (_c_i64, [_c_map]),
+    "pdb_det_batch_map_u32": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_vp, _c_i32, _c_map, _c_i64, _c_i64, _c_vp,
+                                       _c_vp, _c_size, _c_vp]),
+    "pdb_eval_det_fused_map_u32": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_i32, _c_i32, _c_i32, _c_vp, _c_i32, _c_map,
+                                            _c_i64, _c_i64, _c_vp, _c_vp, _c_size, _c_vp]),
+    "pdb_grid_expand_u32": (_c_i32, [_c_vp, _c_vp, _c_vp, _c_map, _c_vp]),
     "pdb_condense_u32": (_c_i32, [_c_vp, _c_vp, _c_i32, _c_vp, _c_vp, _c_vp, _c_vp, _c_size, _c_vp]),
     "pdb_crt_limbs": (_c_i32, [_c_i32]),
     "pdb_crt_scratch_bytes": (_c_size, [_c_i32]),
@@ -234,6 +251,54 @@ def eval_det_fused(ctx: PrimeContext, partial, outer: int, ncoef: int, entries: 
                                      ptr(ids), int(r), int(node_lo), int(nodes), ptr(out), ptr(scratch),
                                      scratch.numel() * scratch.element_size(), stream_handle(stream)),
           "fused det")
+
+
+def node_map(dims, kept_u):
+    """pdb_node_map for a grid of shape dims keeping u < kept_u[a] on each axis
+    with kept_u[a] > 0 (None for the identity)."""
+    if not any(kept_u):
+        return None
+    if len(dims) > MAP_MAX_DIMS:
+        raise ValueError("node maps support at most %d axes" % MAP_MAX_DIMS)
+    m = NodeMapC()
+    m.ndim = len(dims)
+    for a, (n, u) in enumerate(zip(dims, kept_u)):
+        m.dims[a] = int(n)
+        m.kept_u[a] = int(u)
+    return m
+
+
+def node_map_size(m) -> int:
+    n = int(load_library().pdb_node_map_size(ctypes.byref(m)))
+    if n < 0:
+        check(-2, "node map")
+    return n
+
+
+def det_batch_map(ctx: PrimeContext, grids, grid_stride: int, ids, r: int, nmap, node_lo: int, nodes: int,
+                  out, scratch, stream=None):
+    """det_batch over compact nodes [node_lo, node_lo + nodes) of `nmap` (u32 path)."""
+    lib = load_library()
+    check(lib.pdb_det_batch_map_u32(ctx.handle, ptr(grids), int(grid_stride), ptr(ids), int(r), ctypes.byref(nmap),
+                                    int(node_lo), int(nodes), ptr(out), ptr(scratch),
+                                    scratch.numel() * scratch.element_size(), stream_handle(stream)), "det")
+
+
+def eval_det_fused_map(ctx: PrimeContext, partial, outer: int, ncoef: int, entries: int, n_last: int, ids, r: int,
+                       nmap, node_lo: int, nodes: int, out, scratch, stream=None):
+    lib = load_library()
+    check(lib.pdb_eval_det_fused_map_u32(ctx.handle, ptr(partial), int(outer), int(ncoef), int(entries),
+                                         int(n_last), ptr(ids), int(r), ctypes.byref(nmap), int(node_lo),
+                                         int(nodes), ptr(out), ptr(scratch),
+                                         scratch.numel() * scratch.element_size(), stream_handle(stream)),
+          "fused det")
+
+
+def grid_expand(ctx: PrimeContext, compact, grid, nmap, stream=None):
+    """Determinants at the kept nodes of nmap -> every node of the grid."""
+    lib = load_library()
+    check(lib.pdb_grid_expand_u32(ctx.handle, ptr(compact), ptr(grid), ctypes.byref(nmap), stream_handle(stream)),
+          "grid expand")
 
 
 def condense(ctx: PrimeContext, mat, r: int, trail_vals, trail_cols, det_out, scratch, stream=None):

@@ -357,7 +357,115 @@ def c3_full():
                               "workers": os.cpu_count()})
 
 
+def acceptance_exact():
+    """The reference's acceptance sweeps AC3, AC5 and AC6 replayed AS WRITTEN
+    (`test_acceptance.py:89-103`, `:133-156`, `:159-187`): same generators,
+    seeds, trial counts and primes.  The expected values are the reference
+    library's own outputs (AC3: `run(m).terms()`, which the reference test
+    asserts equals `sym_det`; AC5: `det_mod`; AC6: the integers themselves,
+    asserted to round-trip through `combine_tensor`)."""
+    import math
+    from oracles import laplace_det_mod
+    out = {"ac3": [], "ac5": [], "ac6": []}
+    rng = random.Random(20250808)
+    for trial in range(200):
+        r = rng.randint(1, 5)
+        vn = rng.randint(1, 3)
+        max_terms = 4 if r * vn >= 12 else 6
+        rows = random_matrix_terms(rng, r, vn, 4, 100, max_terms)
+        m = ref.poly_matrix(rows, tuple(f"v{i}" for i in range(vn)))
+        got = ref.run(m)
+        out["ac3"].append({"trial": trial, "input": m.to_dict(), "shape": list(got.shape),
+                           "terms": _terms_json(got.terms())})
+    rng = random.Random(5)
+    specs = [ref.find_fourier_primes(1, 1, start=5, min_count=1)[0],
+             ref.find_fourier_primes(4, 1, start=97, min_count=1)[0],
+             ref.PrimeSpec(2013265921, 15, 27, ref.find_root_of_order(2013265921, 1 << 27)),
+             ref.PrimeSpec(1811939329, 27, 26, ref.find_root_of_order(1811939329, 1 << 26))]
+    for trial in range(520):
+        spec = specs[trial % len(specs)]
+        r = rng.randint(1, 6)
+        rows = [[rng.randrange(spec.p) for _ in range(r)] for _ in range(r)]
+        if trial % 3 == 0:
+            for _ in range(r):
+                rows[rng.randrange(r)][rng.randrange(r)] = 0
+            rows[rng.randrange(r)][0] = 0
+        if trial % 7 == 0 and r >= 2:
+            rows[1] = rows[0][:]
+        want = ref.det_mod(ref.ModMatrix.from_rows(rows, spec))
+        assert want == laplace_det_mod(rows, spec.p)
+        out["ac5"].append({"prime": [spec.p, spec.c, spec.q, spec.omega], "rows": rows, "det": int(want)})
+    rng = random.Random(6)
+    pool = [3, 5, 7, 11, 97, 65537, 1000000007, 1000000009, 2013265921, 1811939329]
+    for _ in range(25):
+        primes = rng.sample(pool, rng.randint(2, 6))
+        product = math.prod(primes)
+        values = [rng.randint(-(product - 1) // 2, product // 2) for _ in range(40)]
+        specs = []
+        for p in primes:
+            q = (p - 1) & -(p - 1)
+            specs.append([p, (p - 1) // q, q.bit_length() - 1, ref.find_root_of_order(p, q)])
+        tensors = [ref.reduce_mod(ref.CoeffTensor((40,), tuple(values), ("x",)), ref.PrimeSpec(*s)) for s in specs]
+        assert list(ref.combine_tensor(tensors).coeffs) == values
+        out["ac6"].append({"primes": specs, "values": [str(v) for v in values],
+                           "residues": [[int(v) for v in t.residues] for t in tensors]})
+    _write("acceptance.json", out)
+
+
+C4_RUNGS = {
+    # name: (builder args, keep all terms in the fixture?)
+    "C4_4src_T5T11": ((4, (5, 11), False), True),
+    "C4_4src_T5T11_m": ((4, (5, 11), True), False),     # "c4a": 128^3, 10 primes
+    "C4_5src_T7T11": ((5, (7, 11), False), False),      # "c4b": 128^3, 16 primes
+    "C4_5src_T5T7_m": ((5, (5, 7), True), False),       # 64^4, 7 primes (largest rung)
+    "C2w": (None, True),                                # C2 with coefficients U[-2^31, 2^31]
+}
+
+
+def _result_fixture(name, m, cfg, keep_terms):
+    rm = _ref_matrix(m)
+    t0 = time.time()
+    result, timings, pl = ref.run_report(rm, _ref_cfg(cfg, workers=os.cpu_count()))
+    wall = time.time() - t0
+    coeffs = list(result.coeffs)
+    blob = repr((tuple(result.shape), tuple(coeffs), tuple(result.axis_vars))).encode()
+    nz = [i for i, c in enumerate(coeffs) if c]
+    rng = random.Random(16)
+    picks = sorted(rng.sample(nz, min(64, len(nz)))) + [0, len(coeffs) - 1]
+    rec = {"name": name, "digest": pl.digest(), "input_digest": ref.workspace.digest_of(rm.to_dict()),
+           "shape": list(result.shape), "primes": len(pl.primes), "r": rm.r, "k": rm.k,
+           "sha256": hashlib.sha256(blob).hexdigest(), "nonzero": len(nz),
+           "max_bits": max(abs(c).bit_length() for c in coeffs),
+           "samples": [[i, str(coeffs[i])] for i in picks],
+           "reference_seconds": wall, "timings": timings.as_dict(), "workers": os.cpu_count()}
+    if keep_terms:
+        rec["terms"] = _terms_json(result.terms())
+    print(name, "reference run", round(wall, 1), "s", flush=True)
+    return rec
+
+
+def c4_full(names=None):
+    """The C4 ladder (and C2-wide) end to end through the reference with all host
+    cores; one fixture per rung so that a partially finished ladder is still kept."""
+    path = HERE / "c4_results.json"
+    have = json.loads(path.read_text()) if path.exists() else {}
+    for name, (args, keep) in C4_RUNGS.items():
+        if names and name not in names:
+            continue
+        if name in have:
+            continue
+        m, cfg = workloads.c2(True) if args is None else workloads.harmonic(*args)
+        have[name] = _result_fixture(name, m, cfg, keep)
+        _write("c4_results.json", have)
+
+
 if __name__ == "__main__":
+    if "--acceptance" in sys.argv:
+        acceptance_exact()
+        sys.exit(0)
+    if "--c4" in sys.argv:
+        c4_full([a for a in sys.argv[2:] if not a.startswith("--")] or None)
+        sys.exit(0)
     plans()
     primes()
     wide_cases()
