@@ -137,6 +137,21 @@ int32_t pdb_crt_mrc_u32(const uint32_t* residues, int32_t nprimes, int64_t n, in
                         const uint32_t* primes, uint32_t* limbs, int32_t L, uint8_t* neg,
                         void* scratch, size_t scratch_bytes, void* stream);
 
+/* Positions whose coefficient is nonzero, i.e. some residue is nonzero
+ * (0 <= X < P): index[0..*count) ascending (index has room for n entries;
+ * count is a DEVICE int64).  Replaces the reference's zero test of
+ * CoeffTensor.terms() (tensor.py:101-107) before the lift. */
+size_t pdb_crt_nonzero_scratch_bytes(int64_t n);
+int32_t pdb_crt_nonzero_u32(const uint32_t* residues, int32_t nprimes, int64_t n, int64_t stride,
+                            int64_t* index, int64_t* count, void* scratch, size_t scratch_bytes,
+                            void* stream);
+/* pdb_crt_mrc_u32 at the positions index[0..count) (NULL: 0..count-1), compact
+ * output limbs[i*L + l], neg[i]; *width (DEVICE int32, may be NULL) = the most
+ * limbs any of these coefficients uses.  No host synchronisation. */
+int32_t pdb_crt_mrc_sel_u32(const uint32_t* residues, int32_t nprimes, int64_t stride,
+                            const uint32_t* primes, const int64_t* index, int64_t count, uint32_t* limbs,
+                            int32_t L, uint8_t* neg, int32_t* width, void* stream);
+
 /* Integer-pipe peak of an update primitive (no memory traffic), in updates/s.
  * variant 0 = Shoup mul-mod + sub-mod, 1 = delayed 64-bit MAC (8 per REDC). */
 int32_t pdb_mulmod_peak(uint32_t p, int32_t variant, double* updates_per_second, void* stream);

@@ -116,6 +116,24 @@ def device_lift(residues_dev, primes, n: int, stride: int) -> list:
         raise ValueError("residue rows must be %s for this prime set" % native.word_dtype(wide))
     L = native.crt_limbs(P, wide)
     dev = residues_dev.device
+    host = native.host_module()
+    if not wide:
+        # the library finds the nonzero coefficients (some residue != 0), lifts
+        # only those into compact limb rows and reports the widest; only the used
+        # limbs of the nonzero rows cross to the host
+        idx = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        native.crt_nonzero(residues_dev, P, n, stride, idx, cnt)
+        count = int(cnt.item())
+        limbs = torch.empty((max(count, 1), L), dtype=torch.int32, device=dev)
+        neg = torch.empty(max(count, 1), dtype=torch.uint8, device=dev)
+        wbuf = torch.zeros(1, dtype=torch.int32, device=dev)
+        native.crt_mrc_sel(residues_dev, P, stride, primes, idx, count, limbs, L, neg, wbuf)
+        width = max(int(wbuf.item()), 1)
+        idx_h = np.ascontiguousarray(idx[:count].cpu().numpy())
+        neg_h = np.ascontiguousarray(neg[:count].cpu().numpy())
+        with _PIN_LOCK:   # the staging buffer is shared; the ints are built before it is reused
+            return host.ints_from_limbs(_to_host(limbs[:count, :width]), idx_h, neg_h, int(n), int(width))
     limbs = torch.empty((n, L), dtype=torch.int32, device=dev)
     neg = torch.empty(n, dtype=torch.uint8, device=dev)
     scratch = native.scratch_tensor(native.crt_scratch_bytes(P, wide), dev)
@@ -127,7 +145,6 @@ def device_lift(residues_dev, primes, n: int, stride: int) -> list:
     del used
     sel = limbs.index_select(0, idx)[:, :width].contiguous()
     sel_neg = neg.index_select(0, idx)
-    host = native.host_module()
     idx_h = np.ascontiguousarray(idx.cpu().numpy())
     neg_h = np.ascontiguousarray(sel_neg.cpu().numpy())
     with _PIN_LOCK:   # the staging buffer is shared; the ints are built before it is reused
@@ -145,13 +162,13 @@ def _to_host(t):
     torch = native._torch()
     nbytes = t.numel() * t.element_size()
     if nbytes < (8 << 20) or t.device.type != "cuda":
-        return np.ascontiguousarray(t.cpu().numpy())
+        return np.ascontiguousarray(t.contiguous().cpu().numpy())
     buf = _PINNED.get(t.device.index)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 28), dtype=torch.uint8, pin_memory=True)
         _PINNED[t.device.index] = buf
     view = buf[:nbytes].view(t.dtype).view(t.shape)
-    view.copy_(t)
+    view.copy_(t.contiguous())
     return view.numpy()
 
 

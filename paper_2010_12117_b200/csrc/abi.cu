@@ -119,6 +119,12 @@ int reduce_scatter(PrimeCtx* ctx, const uint32_t* mag, const uint8_t* neg, const
 int condense_run(PrimeCtx* ctx, const uint32_t* mat, int r, uint32_t* trail_vals, int32_t* trail_cols,
                  uint32_t* det_out, void* scratch, size_t scratch_bytes, cudaStream_t st);
 size_t crt_scratch_bytes(int P);
+size_t crt_nonzero_scratch_bytes(int64_t n);
+int crt_nonzero(const uint32_t* res, int P, int64_t n, int64_t stride, int64_t* index, int64_t* count,
+                void* scratch, size_t scratch_bytes, cudaStream_t st);
+int crt_mrc_sel(const uint32_t* res, int P, const int64_t* index, int64_t count, int64_t res_stride,
+                const uint32_t* primes_host, uint32_t* limbs, int L, uint8_t* neg, int32_t* width, int sms,
+                cudaStream_t st);
 int crt_limbs(int P);
 int grid_expand(PrimeCtx* ctx, const uint32_t* compact, uint32_t* grid, const NodeMap& map, const int64_t* dims,
                 cudaStream_t st);
@@ -425,6 +431,24 @@ int32_t pdb_crt_mrc_u32(const uint32_t* residues, int32_t nprimes, int64_t n, in
   int sms = pdb_device_sm_count(dev);
   return crt_mrc(residues, nprimes, n, stride, primes, limbs, L, neg, scratch, scratch_bytes,
                  sms > 0 ? sms : 148, (cudaStream_t)stream);
+}
+
+size_t pdb_crt_nonzero_scratch_bytes(int64_t n) { return crt_nonzero_scratch_bytes(n); }
+
+int32_t pdb_crt_nonzero_u32(const uint32_t* residues, int32_t nprimes, int64_t n, int64_t stride,
+                            int64_t* index, int64_t* count, void* scratch, size_t scratch_bytes,
+                            void* stream) {
+  return crt_nonzero(residues, nprimes, n, stride, index, count, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int32_t pdb_crt_mrc_sel_u32(const uint32_t* residues, int32_t nprimes, int64_t stride,
+                            const uint32_t* primes, const int64_t* index, int64_t count, uint32_t* limbs,
+                            int32_t L, uint8_t* neg, int32_t* width, void* stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int sms = pdb_device_sm_count(dev);
+  return crt_mrc_sel(residues, nprimes, index, count, stride, primes, limbs, L, neg, width, sms > 0 ? sms : 148,
+                     (cudaStream_t)stream);
 }
 
 int32_t pdb_mulmod_peak(uint32_t p, int32_t variant, double* ups, void* stream) {

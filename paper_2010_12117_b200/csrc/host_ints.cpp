@@ -15,11 +15,14 @@
 #include <cstdint>
 #include <cstring>
 
+// On other interpreters (or with PDB_NO_DIRECT_LONG) every coefficient takes the
+// portable path below, which uses the public API only.
 // CPython 3.12/3.13 store an int as 30-bit digits behind a tag word
 // (digit count << 3 | sign: 0 positive, 2 negative).  Building the object
 // directly from the limb bit stream skips _PyLong_FromByteArray's byte loop
 // and, for negative values, the second allocation of PyNumber_Negative.
-#if PY_VERSION_HEX >= 0x030C0000 && PY_VERSION_HEX < 0x030E0000 && PYLONG_BITS_IN_DIGIT == 30
+#if PY_VERSION_HEX >= 0x030C0000 && PY_VERSION_HEX < 0x030E0000 && PYLONG_BITS_IN_DIGIT == 30 && \
+    !defined(PDB_NO_DIRECT_LONG)
 #define PDB_DIRECT_LONG 1
 static PyObject* long_from_limbs(const unsigned char* row, Py_ssize_t width, bool negative) {
   digit buf[80];   // up to 74 limbs = 2368 bits
@@ -51,19 +54,30 @@ static PyObject* long_from_limbs(const unsigned char* row, Py_ssize_t width, boo
 }
 #endif
 
-// One coefficient: |value| as `width` little-endian u32 limbs, then the sign.
-static PyObject* make_int(const unsigned char* row, Py_ssize_t width, bool negative) {
-#ifdef PDB_DIRECT_LONG
-  if (width <= 74) return long_from_limbs(row, width, negative);
-#endif
-  PyObject* v;
+// Portable path (public API only, any CPython): int.from_bytes(row, "little").
+static PyObject* g_from_bytes = nullptr;   // bound method int.from_bytes
+
+static PyObject* portable_int(const unsigned char* row, Py_ssize_t width) {
   if (width <= 2) {
     uint64_t mag = 0;
     std::memcpy(&mag, row, (size_t)width * 4);
-    v = PyLong_FromUnsignedLongLong(mag);
-  } else {
-    v = _PyLong_FromByteArray(row, (size_t)width * 4, /*little_endian=*/1, /*is_signed=*/0);
+    return PyLong_FromUnsignedLongLong(mag);
   }
+  if (!g_from_bytes) {
+    g_from_bytes = PyObject_GetAttrString((PyObject*)&PyLong_Type, "from_bytes");
+    if (!g_from_bytes) return nullptr;
+  }
+  return PyObject_CallFunction(g_from_bytes, "y#s", (const char*)row, width * 4, "little");
+}
+
+// One coefficient: |value| as `width` little-endian u32 limbs, then the sign.
+static PyObject* make_int(const unsigned char* row, Py_ssize_t width, bool negative, bool portable) {
+#ifdef PDB_DIRECT_LONG
+  if (!portable && width <= 74) return long_from_limbs(row, width, negative);
+#else
+  (void)portable;
+#endif
+  PyObject* v = portable_int(row, width);
   if (v && negative) {
     PyObject* m = PyNumber_Negative(v);
     Py_DECREF(v);
@@ -72,7 +86,7 @@ static PyObject* make_int(const unsigned char* row, Py_ssize_t width, bool negat
   return v;
 }
 
-static PyObject* ints_from_limbs(PyObject*, PyObject* args) {
+static PyObject* build(PyObject* args, bool portable) {
   Py_buffer limbs, index, neg;
   Py_ssize_t n, width;
   if (!PyArg_ParseTuple(args, "y*y*y*nn", &limbs, &index, &neg, &n, &width)) return nullptr;
@@ -103,7 +117,7 @@ static PyObject* ints_from_limbs(PyObject*, PyObject* args) {
     for (Py_ssize_t i = 0; i < n; ++i) {
       PyObject* v;
       if (j < count && ix[j] == i) {
-        v = make_int(lb + (size_t)j * (size_t)width * 4, width, ng[j] != 0);
+        v = make_int(lb + (size_t)j * (size_t)width * 4, width, ng[j] != 0, portable);
         ++j;
         if (!v) { Py_CLEAR(out); goto done; }
       } else {
@@ -118,7 +132,7 @@ static PyObject* ints_from_limbs(PyObject*, PyObject* args) {
       PyTuple_SET_ITEM(out, i, zero);
     }
     for (Py_ssize_t j = 0; j < count; ++j) {
-      PyObject* v = make_int(lb + (size_t)j * (size_t)width * 4, width, ng[j] != 0);
+      PyObject* v = make_int(lb + (size_t)j * (size_t)width * 4, width, ng[j] != 0, portable);
       if (!v) { Py_CLEAR(out); goto done; }
       PyObject* old = PyTuple_GET_ITEM(out, ix[j]);
       PyTuple_SET_ITEM(out, ix[j], v);
@@ -133,9 +147,23 @@ done:
   return out;
 }
 
+static PyObject* ints_from_limbs(PyObject*, PyObject* args) { return build(args, false); }
+static PyObject* ints_from_limbs_portable(PyObject*, PyObject* args) { return build(args, true); }
+
+static PyObject* direct_path(PyObject*, PyObject*) {
+#ifdef PDB_DIRECT_LONG
+  Py_RETURN_TRUE;
+#else
+  Py_RETURN_FALSE;
+#endif
+}
+
 static PyMethodDef methods[] = {
     {"ints_from_limbs", ints_from_limbs, METH_VARARGS,
      "ints_from_limbs(limbs, index, neg, n, width) -> tuple of n Python ints"},
+    {"ints_from_limbs_portable", ints_from_limbs_portable, METH_VARARGS,
+     "the same through the public C API only (int.from_bytes): the path on other CPython ABIs"},
+    {"direct_path", direct_path, METH_NOARGS, "True if this build writes PyLong digits directly"},
     {nullptr, nullptr, 0, nullptr}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_pdb_host", "native result materialisation", -1, methods};

@@ -70,6 +70,10 @@ _SIGNATURES = {
     "pdb_crt_scratch_bytes": (_c_size, [_c_i32]),
     "pdb_crt_mrc_u32": (_c_i32, [_c_vp, _c_i32, _c_i64, _c_i64, _c_vp, _c_vp, _c_i32, _c_vp, _c_vp,
                                  _c_size, _c_vp]),
+    "pdb_crt_nonzero_scratch_bytes": (_c_size, [_c_i64]),
+    "pdb_crt_nonzero_u32": (_c_i32, [_c_vp, _c_i32, _c_i64, _c_i64, _c_vp, _c_vp, _c_vp, _c_size, _c_vp]),
+    "pdb_crt_mrc_sel_u32": (_c_i32, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp, _c_i64, _c_vp, _c_i32, _c_vp, _c_vp,
+                                     _c_vp]),
     "pdb_mulmod_peak": (_c_i32, [_c_u32, _c_i32, ctypes.POINTER(ctypes.c_double), _c_vp]),
     # the wide path (2^31 <= p < 2^62): u64 twins
     "pdb_prime_ctx_create_wide": (_c_i32, [_c_u64, _c_u64, _c_i32, ctypes.POINTER(_c_vp)]),
@@ -329,6 +333,28 @@ def crt_mrc(residues, nprimes: int, n: int, stride: int, primes, limbs, L: int, 
         fn = lib.pdb_crt_mrc_u32
     check(fn(ptr(residues), int(nprimes), int(n), int(stride), hp, ptr(limbs), int(L), ptr(neg), ptr(scratch),
              scratch.numel() * scratch.element_size(), stream_handle(stream)), "crt")
+
+
+def crt_nonzero(residues, nprimes: int, n: int, stride: int, index, count, stream=None):
+    """Ascending positions < n with a nonzero residue row -> index; device count."""
+    lib = load_library()
+    torch = _torch()
+    scratch = scratch_tensor(lib.pdb_crt_nonzero_scratch_bytes(int(n)), residues.device)
+    check(lib.pdb_crt_nonzero_u32(ptr(residues), int(nprimes), int(n), int(stride), ptr(index), ptr(count),
+                                  ptr(scratch), scratch.numel() * scratch.element_size(), stream_handle(stream)),
+          "crt nonzero")
+    del torch
+
+
+def crt_mrc_sel(residues, nprimes: int, stride: int, primes, index, count: int, limbs, L: int, neg, width,
+                stream=None):
+    """CRT lift at positions index[0..count) (index None: 0..count-1), compact output."""
+    lib = load_library()
+    hp = (ctypes.c_uint32 * nprimes)(*[int(p) for p in primes])
+    check(lib.pdb_crt_mrc_sel_u32(ptr(residues), int(nprimes), int(stride), hp,
+                                  ptr(index) if index is not None else None, int(count), ptr(limbs), int(L),
+                                  ptr(neg), ptr(width) if width is not None else None, stream_handle(stream)),
+          "crt")
 
 
 def launch_count() -> int:

@@ -1,0 +1,41 @@
+"""The native host module (_pdb_host, csrc/host_ints.cpp) that turns the GPU
+CRT's limb rows into Python ints: the direct-PyLong path (CPython 3.12/3.13)
+and the portable public-API path (any other interpreter) must agree with
+int.from_bytes on every magnitude and sign (CPU test)."""
+
+import random
+
+import numpy as np
+import pytest
+
+from paper_2010_12117_b200 import native
+
+
+@pytest.mark.parametrize("width", [1, 2, 3, 15, 24, 80])
+@pytest.mark.parametrize("ordered", [True, False])
+def test_both_paths_equal_int_from_bytes(width, ordered):
+    host = native.host_module()
+    rng = random.Random(width)
+    n = 2000
+    idx = sorted(rng.sample(range(n), 500))
+    if not ordered:
+        rng.shuffle(idx)
+    bits = [rng.choice([0, 1, 29, 30, 31, 32, 59, 60, 61, 63, 64, 65, 32 * width]) for _ in idx]
+    vals = [rng.getrandbits(min(b, 32 * width)) for b in bits]
+    limbs = np.frombuffer(b"".join(v.to_bytes(4 * width, "little") for v in vals), dtype="<u4").reshape(-1, width)
+    neg = np.array([rng.random() < 0.5 for _ in idx], dtype=np.uint8)
+    ix = np.array(idx, dtype=np.int64)
+    want = [0] * n
+    for i, v, s in zip(idx, vals, neg):
+        want[i] = -v if s else v
+    assert host.ints_from_limbs(limbs, ix, neg, n, width) == tuple(want)
+    assert host.ints_from_limbs_portable(limbs, ix, neg, n, width) == tuple(want)
+
+
+def test_rejects_inconsistent_buffers():
+    host = native.host_module()
+    limbs = np.zeros((3, 2), dtype=np.uint32)
+    with pytest.raises(ValueError):
+        host.ints_from_limbs(limbs, np.arange(2, dtype=np.int64), np.zeros(2, dtype=np.uint8), 5, 2)
+    with pytest.raises(IndexError):
+        host.ints_from_limbs(limbs, np.array([0, 1, 9], dtype=np.int64), np.zeros(3, dtype=np.uint8), 5, 2)
