@@ -153,7 +153,9 @@ int32_t pdb_crt_mrc_sel_u32(const uint32_t* residues, int32_t nprimes, int64_t s
                             int32_t L, uint8_t* neg, int32_t* width, void* stream);
 
 /* Integer-pipe peak of an update primitive (no memory traffic), in updates/s.
- * variant 0 = Shoup mul-mod + sub-mod, 1 = delayed 64-bit MAC (8 per REDC). */
+ * variant 0 = Shoup mul-mod + sub-mod, 1 = delayed 64-bit MAC (9 MACs + one REDC,
+ * the det kernel's trailing update: updates = MACs), 2 = raw accumulating
+ * IMAD.WIDE stream (the integer multiplier's ceiling, MACs/s). */
 int32_t pdb_mulmod_peak(uint32_t p, int32_t variant, double* updates_per_second, void* stream);
 
 /* ---- the wide path: primes 2^31 <= p < 2^62 --------------

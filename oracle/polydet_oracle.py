@@ -214,7 +214,13 @@ def run_pipeline(unique_terms, entry_ids, r, shape, primes, workers=1):
     """
     residues = []
     for p, omega, q in primes:
-        grids = [ntt_multi(reduce_entry(t, shape, p), shape, p, omega, q) for t in unique_terms]
+        if workers > 1:   # the reference's forward stage maps entries over its worker pool (pipeline.py:364)
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(workers) as ex:
+                grids = list(ex.map(lambda t: ntt_multi(reduce_entry(t, shape, p), shape, p, omega, q),
+                                    unique_terms))
+        else:
+            grids = [ntt_multi(reduce_entry(t, shape, p), shape, p, omega, q) for t in unique_terms]
         values = det_grid(grids, r, p, entry_ids, workers=workers)
         residues.append(ntt_multi(values, shape, p, omega, q, inverse=True))
     return crt_combine(residues, [p for p, _, _ in primes]), residues

@@ -151,6 +151,37 @@ def device_lift(residues_dev, primes, n: int, stride: int) -> list:
         return host.ints_from_limbs(_to_host(sel), idx_h, neg_h, int(n), int(width))
 
 
+def sharded_lift(block, primes, n: int, lo: int, rank: int, size: int) -> tuple:
+    """Multi-GPU CRT (shard.py): `block` holds every prime's residues [P][m] of
+    this rank's coefficient range [lo, lo + m); each rank compacts and lifts its
+    range, the compact limb rows are all-gathered, and every rank builds the
+    same tuple of n Python ints (u32 prime sets)."""
+    from . import shard
+
+    torch = native._torch()
+    P, m = block.shape
+    dev = block.device
+    block = block.contiguous()
+    idx = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    native.crt_nonzero(block, P, m, m, idx, cnt)
+    count = int(cnt.item())
+    L = native.crt_limbs(P)
+    limbs = torch.empty((max(count, 1), L), dtype=torch.int32, device=dev)
+    neg = torch.empty(max(count, 1), dtype=torch.uint8, device=dev)
+    wbuf = torch.zeros(1, dtype=torch.int32, device=dev)
+    native.crt_mrc_sel(block, P, m, primes, idx, count, limbs, L, neg, wbuf)
+    import torch.distributed as dist
+    dist.all_reduce(wbuf, op=dist.ReduceOp.MAX)
+    width = max(int(wbuf.item()), 1)
+    idx[:count] += lo
+    g_limbs, g_idx, g_neg = shard.gather_compact(count, limbs, idx, neg, width, rank, size)
+    idx_h = np.ascontiguousarray(g_idx.cpu().numpy())
+    neg_h = np.ascontiguousarray(g_neg.cpu().numpy())
+    with _PIN_LOCK:
+        return native.host_module().ints_from_limbs(_to_host(g_limbs), idx_h, neg_h, int(n), int(width))
+
+
 _PINNED = {}
 _PIN_LOCK = threading.Lock()
 

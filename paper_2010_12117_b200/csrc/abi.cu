@@ -215,6 +215,26 @@ __global__ void peak_delayed(uint32_t* out, uint32_t seed, Mod32 m, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// The raw integer-multiplier ceiling: a stream of independent accumulating
+// 32x32->64 IMAD.WIDE (8 chains per thread; the multiplier changes every
+// iteration so no product can be hoisted).
+__global__ void peak_imadwide(uint32_t* out, uint32_t seed, int iters) {
+  uint64_t acc[8];
+  uint32_t x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { acc[i] = i; x[i] = seed * (i + 1) + threadIdx.x; }
+  uint32_t y = seed ^ (threadIdx.x * 2654435761u);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = mad_wide(x[i], y, acc[i]);
+    y += 0x9e3779b9u;
+  }
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s ^= acc[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (uint32_t)(s ^ (s >> 32));
+}
+
 }  // namespace pdb
 
 using namespace pdb;
@@ -469,7 +489,8 @@ int32_t pdb_mulmod_peak(uint32_t p, int32_t variant, double* ups, void* stream) 
   for (int rep = 0; rep < 4; ++rep) {
     cudaEventRecord(e0, st);
     if (variant == 0) peak_shoup<<<blocks, threads, 0, st>>>(d, 12345u + rep, w, ws, p, iters);
-    else peak_delayed<<<blocks, threads, 0, st>>>(d, 12345u + rep, m, iters / 8);
+    else if (variant == 1) peak_delayed<<<blocks, threads, 0, st>>>(d, 12345u + rep, m, iters / 8);
+    else peak_imadwide<<<blocks, threads, 0, st>>>(d, 12345u + rep, iters);
     cudaEventRecord(e1, st);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -479,7 +500,7 @@ int32_t pdb_mulmod_peak(uint32_t p, int32_t variant, double* ups, void* stream) 
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(d);
-  const double per_thread = variant == 0 ? 8.0 * iters : 4.0 * 9 * (iters / 8);
+  const double per_thread = variant == 0 ? 8.0 * iters : (variant == 1 ? 4.0 * 9 * (iters / 8) : 8.0 * iters);
   *ups = per_thread * threads * blocks / (best * 1e-3);
   return check_launch("peak");
 }

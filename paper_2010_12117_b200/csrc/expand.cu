@@ -61,8 +61,10 @@ static const ExpandTables* expand_tables(PrimeCtx* ctx, int N, int U) {
       h[64 + a * 8 + b] = (uint32_t)mulm(powm(w8, (uint64_t)a * b, p), R, p);             // [v][l]
     }
   // Lagrange basis on y_u = w^(8u), u < U, evaluated at y_u', u' = U..N8-1
-  std::vector<uint64_t> y(N8), bw(U);
-  for (int j = 0; j < N8; ++j) y[j] = powm(w, 8ull * j, p);
+  std::vector<uint64_t> wp(N), y(N8), bw(U);
+  wp[0] = 1 % p;
+  for (int j = 1; j < N; ++j) wp[j] = mulm(wp[j - 1], w, p);
+  for (int j = 0; j < N8; ++j) y[j] = wp[8 * j];
   for (int u = 0; u < U; ++u) {
     uint64_t d = 1;
     for (int j = 0; j < U; ++j)
@@ -76,7 +78,7 @@ static const ExpandTables* expand_tables(PrimeCtx* ctx, int N, int U) {
     for (int u = 0; u < U; ++u) {
       const uint64_t Lu = mulm(mulm(ell, bw[u], p), powm((yt + p - y[u]) % p, p - 2, p), p);
       for (int ll = 0; ll < 8; ++ll) {
-        const uint64_t tw = powm(w, (uint64_t)ll * (uint64_t)(U + t - u), p);
+        const uint64_t tw = wp[((uint64_t)ll * (uint64_t)(U + t - u)) % N];
         h[128 + ((size_t)ll * T + t) * U + u] = (uint32_t)mulm(mulm(tw, Lu, p), R, p);
       }
     }

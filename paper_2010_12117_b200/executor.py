@@ -39,7 +39,7 @@ import numpy as np
 
 from . import native, shard
 from .checkpoint import Workspace, digest_of
-from .crt import device_lift, wide_primes
+from .crt import device_lift, sharded_lift, wide_primes
 from .errors import StaleWorkspaceError
 from .layout import CoeffTensor, PolyMatrix, residue_dtype
 from .planner import Plan, PipelineConfig, StageTimings, degree_bound, plan
@@ -337,15 +337,30 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
         if ws is not None:
             ws.store_residues(unit, native.to_host_words(residues[row], dp.wide), pl.shape)
         cfg._notify(unit)
-    if size > 1:
-        residues = shard.gather_residues(residues, whole, rank, size)
+    primes = [s.p for s in pl.primes]
+    if size > 1 and not dp.wide:
+        # sharded CRT: every prime's residues of my coefficient range (all-to-all),
+        # lifted here; the compact results are all-gathered (crt.sharded_lift)
+        lo, hi = shard.coefficient_range(nodes, rank, size)
+        block = shard.exchange_residues(residues, whole, rank, size) if whole else None
         if slab_primes:
             slab_rows = _slab_primes(dp, slab_primes, work, det_buf, scratch, det_chunk, rank, size, cfg, events,
                                      torch, stream)
-            residues = torch.cat([residues, slab_rows]) if whole else slab_rows
-    t4 = _Timer(torch, stream).mark()
-    coeffs = device_lift(residues, [s.p for s in pl.primes], nodes, nodes)
-    t5 = _Timer(torch, stream).mark()
+            block = torch.cat([block, slab_rows[:, lo:hi]]) if whole else slab_rows[:, lo:hi]
+        del residues
+        t4 = _Timer(torch, stream).mark()
+        coeffs = sharded_lift(block, primes, nodes, lo, rank, size)
+        t5 = _Timer(torch, stream).mark()
+    else:
+        if size > 1:   # u64 residues: gather every row, lift on every rank
+            residues = shard.gather_residues(residues, whole, rank, size)
+            if slab_primes:
+                slab_rows = _slab_primes(dp, slab_primes, work, det_buf, scratch, det_chunk, rank, size, cfg,
+                                         events, torch, stream)
+                residues = torch.cat([residues, slab_rows]) if whole else slab_rows
+        t4 = _Timer(torch, stream).mark()
+        coeffs = device_lift(residues, primes, nodes, nodes)
+        t5 = _Timer(torch, stream).mark()
     torch.cuda.synchronize()
     for t0, t1, t2, t3 in events:
         timings.fft += t0.elapsed_time(t1) / 1e3
@@ -556,6 +571,18 @@ class PrimeStages:
     def determinants(self, pi):
         _det_stage(self.dp, self.ctx(pi), self.work, self.compact, self.scratch, self.chunk, None, pi, self._cfg,
                    self.det)
+
+    def det_kernels(self, pi):
+        """The determinant launches alone: every kept node (dp.sel of them) into
+        `compact` (pruned) or `det` (unpruned)."""
+        dp = self.dp
+        out = self.det if dp.nmap is None else self.compact
+        _det_range(dp, self.ctx(pi), self.work, out, self.scratch, self.chunk, 0, dp.sel)
+
+    def expand(self, pi):
+        """Kept-node determinants -> the full grid in `det` (no-op unpruned)."""
+        if self.dp.nmap is not None:
+            _expand(self.dp, self.ctx(pi), self.compact, self.det)
 
     def interpolate(self, pi):
         native.ntt_multi(self.ctx(pi), self.det, 1, self.dp.shape, None, range(self.dp.vn), True)

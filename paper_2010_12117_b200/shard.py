@@ -12,6 +12,12 @@ gloo in the CPU tests).  Two partitions, combined:
   node range), the slabs are all-gathered into the full determinant grid on
   every rank, and every rank runs that prime's (cheap) inverse NTT.
 
+The CRT is sharded too (the reference does it once over every coefficient,
+crt.py:94-130): an all-to-all leaves rank g with every prime's residues of
+its coefficient range [lo_g, hi_g), it lifts those (nonzero compaction + the
+mixed-radix kernel), and the compact limb rows of all ranks are all-gathered
+so that every rank returns the same Python-int result.
+
 Output is bit-identical for any device count because every residue is a pure
 function of the prime and node (test_multiproc.py, test_gpu_parity.py).
 """
@@ -87,3 +93,74 @@ def gather_residues(local, prime_count: int, rank: int, size: int):
         for j, pi in enumerate(my_primes(prime_count, g, size)):
             order[pi] = g * rows + j
     return full[order.to(full.device)]
+
+
+def coefficient_range(n: int, rank: int, size: int):
+    """[lo, hi) of the n coefficient positions whose CRT `rank` owns."""
+    base, extra = divmod(n, size)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def _backend():
+    import torch.distributed as dist
+    return dist.get_backend()
+
+
+def exchange_residues(local, prime_count: int, rank: int, size: int):
+    """All-to-all of the round-robin residue rows: `local` is this rank's
+    [prime_count / size][n] block (primes rank, rank + size, ...); returns the
+    [prime_count][hi - lo] residues (prime order) of this rank's coefficient
+    range.  NCCL: one all_to_all_single; other backends (gloo in the tests):
+    an all-gather of the ranges, same result."""
+    import torch
+    import torch.distributed as dist
+
+    rows, n = local.shape
+    width = -(-n // size)
+    lo, hi = coefficient_range(n, rank, size)
+    send = local.new_zeros((size, rows, width))
+    for g in range(size):
+        glo, ghi = coefficient_range(n, g, size)
+        send[g, :, : ghi - glo] = local[:, glo:ghi]
+    if _backend() == "nccl":
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv.view(-1), send.view(-1))
+    else:
+        full = local.new_empty((size, size, rows, width))
+        dist.all_gather_into_tensor(full.view(-1), send.view(-1))
+        recv = full[:, rank]
+    out = local.new_empty((prime_count, hi - lo))
+    for g in range(size):
+        for j, pi in enumerate(my_primes(prime_count, g, size)):
+            out[pi] = recv[g, j, : hi - lo]
+    return out
+
+
+def gather_compact(count: int, limbs, idx, neg, width: int, rank: int, size: int):
+    """All-gather every rank's compact CRT output (count rows of `width` limbs,
+    global positions, sign bytes) -> the concatenation in rank order (ascending
+    positions, since the ranges are ascending), on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    dev = limbs.device
+    counts = torch.tensor([count], dtype=torch.int64, device=dev)
+    allc = torch.empty(size, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allc, counts)
+    allc = allc.tolist()
+    mx = max(max(allc), 1)
+    pl = limbs.new_zeros((mx, width))
+    pl[:count] = limbs[:count, :width]
+    pi = idx.new_zeros(mx)
+    pi[:count] = idx[:count]
+    pn = neg.new_zeros(mx)
+    pn[:count] = neg[:count]
+    gl = limbs.new_empty((size, mx, width))
+    gi = idx.new_empty((size, mx))
+    gn = neg.new_empty((size, mx))
+    dist.all_gather_into_tensor(gl.view(-1), pl.view(-1))
+    dist.all_gather_into_tensor(gi.view(-1), pi)
+    dist.all_gather_into_tensor(gn.view(-1), pn)
+    return (torch.cat([gl[g, :c] for g, c in enumerate(allc)]), torch.cat([gi[g, :c] for g, c in enumerate(allc)]),
+            torch.cat([gn[g, :c] for g, c in enumerate(allc)]))

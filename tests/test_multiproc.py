@@ -114,3 +114,56 @@ def test_slab_partition_covers_axis():
             assert spans[0][0] == 0 and spans[-1][1] == n0
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+
+
+def _exchange_worker(rank, size, port, P, n, force_a2a, out_path):
+    """CRT sharding: the all-to-all of residue rows leaves each rank every
+    prime's residues of its coefficient range; the compact CRT rows of all
+    ranks all-gather back into ascending order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    rng = np.random.default_rng(7)
+    full = torch.tensor(rng.integers(0, 2**31 - 1, (P, n)), dtype=torch.int64)
+    whole = (P // size) * size
+    local = full[shard.my_primes(whole, rank, size)]
+    if force_a2a:
+        shard._backend = lambda: "nccl"     # exercise all_to_all_single (gloo implements it on CPU)
+    block = shard.exchange_residues(local, whole, rank, size)
+    lo, hi = shard.coefficient_range(n, rank, size)
+    ok = bool(torch.equal(block, full[:whole, lo:hi]))
+    # compact rows: this rank's "nonzero" positions are those with an odd first residue
+    pos = torch.nonzero(block[0] % 2 == 1).squeeze(1)
+    count = int(pos.numel())
+    width = 3
+    limbs = torch.zeros((max(count, 1), 5), dtype=torch.int32)
+    limbs[:count, 0] = (pos + lo).to(torch.int32)
+    limbs[:count, 2] = rank
+    neg = (pos % 3 == 0).to(torch.uint8)
+    g_l, g_i, g_n = shard.gather_compact(count, limbs, pos + lo, neg, width, rank, size)
+    want_pos = torch.nonzero(full[0] % 2 == 1).squeeze(1) if whole else torch.zeros(0, dtype=torch.int64)
+    ok = ok and torch.equal(g_i, want_pos) and torch.equal(g_l[:, 0].to(torch.int64), want_pos)
+    ok = ok and g_l.shape[1] == width and torch.equal(g_n, ((want_pos - torch.tensor(
+        [shard.coefficient_range(n, g, size)[0] for g in range(size)])[
+            torch.searchsorted(torch.tensor([shard.coefficient_range(n, g, size)[1] for g in range(size)]),
+                               want_pos, right=True)]) % 3 == 0).to(torch.uint8))
+    flag = torch.tensor([1 if ok else 0])
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        np.save(out_path, flag.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("size,P,n,force_a2a", [(2, 22, 1000, False), (3, 23, 1001, False), (5, 23, 64, False),
+                                                (2, 22, 1000, True), (3, 9, 517, True)])
+def test_crt_exchange_and_gather(tmp_path, size, P, n, force_a2a):
+    out = tmp_path / "flag.npy"
+    mp.spawn(_exchange_worker, args=(size, _free_port(), P, n, force_a2a, str(out)), nprocs=size, join=True)
+    assert np.load(out).tolist() == [1]
+
+
+def test_coefficient_ranges_cover():
+    for n in (1, 7, 262144, 16777216):
+        for G in (1, 2, 3, 8):
+            spans = [shard.coefficient_range(n, g, G) for g in range(G)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))

@@ -25,8 +25,9 @@ def digest(res):
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c3"
-    m, cfg = {"c3": workloads.c3, "c1": workloads.c1,
-              "c4a": lambda: workloads.harmonic(4, (5, 11), True)}[name]()
+    m, cfg = {"c3": workloads.c3, "c1": workloads.c1, "c2w": lambda: workloads.c2(True),
+              "c4a": lambda: workloads.harmonic(4, (5, 11), True),
+              "c4_4d": lambda: workloads.harmonic(5, (5, 7), True)}[name]()
     dev = int(os.environ.get("PDB_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(dev)
     single = digest(run(m, cfg))          # before the process group exists: one-process run
