@@ -241,8 +241,31 @@ static int launch_small(int r, Src src, const int32_t* ids, int64_t lo, int64_t 
 }
 
 size_t det_scratch_bytes(int r, int64_t nodes) {
-  (void)r;   // flag count + flagged node list + one denominator per node
-  return 256 + sizeof(int64_t) * (size_t)nodes + sizeof(uint32_t) * ((size_t)nodes + 3);
+  (void)r;   // flag count + flagged node list + one denominator per node + the row table
+  return 256 + sizeof(int64_t) * (size_t)nodes + sizeof(uint32_t) * ((size_t)nodes + 3) +
+         sizeof(int64_t) * ((size_t)nodes / 8 + 2) + 16;
+}
+
+// Full outer index of every compact last-axis row a fused launch touches (pruned maps).
+__global__ void fused_row_table(NodeMap map, int64_t orow0, int64_t rows, int64_t klast, int lognl,
+                                int64_t* __restrict__ table) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < rows; j += (int64_t)gridDim.x * blockDim.x)
+    table[j] = map.full((orow0 + j) * klast) >> lognl;
+}
+
+static void prepare_src(PrimeCtx*, StagedSrc&, char*, int64_t, int64_t, cudaStream_t) {}
+
+static void prepare_src(PrimeCtx* ctx, FusedSrc& src, char* tail, int64_t node_lo, int64_t nodes, cudaStream_t st) {
+  (void)node_lo;
+  if (!src.map.nd || src.ulast < 1) return;
+  const int64_t klast = 8 * (int64_t)src.ulast;
+  const int64_t rows = (nodes + klast - 1) / klast + 1;
+  int64_t* table = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(tail) + 15) & ~uintptr_t(15));
+  const int64_t blocks = (rows + 255) / 256;
+  const int g = (int)(blocks < (int64_t)ctx->sms * 4 ? blocks : (int64_t)ctx->sms * 4);
+  fused_row_table<<<g, 256, 0, st>>>(src.map, src.orow0, rows, klast, __builtin_ctz((unsigned)src.NL), table);
+  count_launch();
+  src.orow_full = table;
 }
 
 template <class Src>
@@ -363,6 +386,7 @@ int det_run(PrimeCtx* ctx, Src src, const int32_t* ids, int r, int64_t node_lo, 
   char* base = static_cast<char*>(scratch);
   FlagList flags{reinterpret_cast<unsigned long long*>(base), reinterpret_cast<int64_t*>(base + 256)};
   uint32_t* den = reinterpret_cast<uint32_t*>(base + 256 + sizeof(int64_t) * (size_t)nodes);
+  prepare_src(ctx, src, reinterpret_cast<char*>(den + nodes + 3), node_lo, nodes, st);
   const Mod32 m = ctx->m;
   bool fast = false;
   if (cudaMemsetAsync(flags.count, 0, sizeof(unsigned long long), st) != cudaSuccess)

@@ -125,24 +125,22 @@ struct GjD8 {
   int64_t orel, o;
   int ublk;
 };
-__device__ __forceinline__ GjD8 gj_d8(const FusedSrc& src, int U, int64_t it, int64_t node_lo) {
-  const int per_o = src.ulast / U;
-  const int64_t klast = 8 * (int64_t)src.ulast;
+// Once per iteration, in 32-bit arithmetic (iterations per launch < 2^32;
+// the launch's first row orow0 comes from the host).
+__device__ __forceinline__ GjD8 gj_d8(const FusedSrc& src, int U, int64_t it) {
+  const uint32_t per_o = (uint32_t)(src.ulast / U);
   GjD8 d;
-  d.orel = it / per_o;
-  d.ublk = (int)(it - d.orel * per_o);
-  const int64_t oc = node_lo / klast + d.orel;   // compact outer row
-  d.o = src.map.nd ? src.map.full(oc * klast) / src.NL : oc;
+  d.orel = (uint32_t)it / per_o;
+  d.ublk = (int)((uint32_t)it - (uint32_t)d.orel * per_o);
+  // full outer index of the row: a table the launcher builds for pruned maps
+  d.o = src.orow_full ? __ldg(src.orow_full + d.orel) : src.orow0 + d.orel;
   return d;
 }
 
-// compact index (relative to the launch) of slot v * U + uu of iteration `it`
-__device__ __forceinline__ int64_t gj_node_dft8(const FusedSrc& src, int64_t it, int slot, const GjGeom& g) {
-  const int per_o = src.ulast / g.U;
-  const int64_t orel = it / per_o;
-  const int ublk = (int)(it - orel * per_o);
+// compact index (relative to the launch) of slot v * U + uu of iteration d8
+__device__ __forceinline__ int64_t gj_node_dft8(const FusedSrc& src, const GjD8& d8, int slot, const GjGeom& g) {
   const int v = slot / g.U, uu = slot - v * g.U;
-  return orel * 8 * (int64_t)src.ulast + (int64_t)v * src.ulast + ublk * g.U + uu;
+  return d8.orel * 8 * (int64_t)src.ulast + (int64_t)v * src.ulast + d8.ublk * g.U + uu;
 }
 
 // ---- fills: the RP x RP matrices of one iteration (padding = Montgomery identity) ----
@@ -191,10 +189,9 @@ __device__ __forceinline__ void gj_fill(const FusedSrc& src, uint32_t* mats, con
 // entries; two positions are kept in flight per thread.
 template <int E>
 __device__ __forceinline__ void gj_fill_dft8_e(const FusedSrc& src, uint32_t* mats, const GjGeom& g,
-                                               const int32_t* ids, int64_t it, int64_t node_lo, uint32_t one) {
+                                               const int32_t* ids, const GjD8& d8, uint32_t one) {
   const int r = g.r, RP = g.RP, S = g.S, U = g.U, NL = src.NL, k = src.k;
   const uint32_t p = src.p;
-  const GjD8 d8 = gj_d8(src, U, it, node_lo);
   const int64_t o = d8.o;
   const int ublk = d8.ublk;
   const int step8 = NL / 8;
@@ -264,11 +261,10 @@ __device__ __forceinline__ void gj_fill_dft8_e(const FusedSrc& src, uint32_t* ma
 // the shared-memory stores and the coefficient loads use immediate offsets.
 template <int E, int UC = 0, int MSC = 0, int NC = 0>
 __device__ __forceinline__ void gj_fill_dft8_dense(const FusedSrc& src, uint32_t* mats, const GjGeom& g,
-                                                   int64_t it, int64_t node_lo) {
+                                                   const GjD8& d8) {
   const int U = UC ? UC : g.U, NL = src.NL, k = src.k, n = NC ? NC : g.r * g.r;
   const int MS = MSC ? MSC : g.MS;
   const uint32_t p = src.p;
-  const GjD8 d8 = gj_d8(src, U, it, node_lo);
   const int64_t o = d8.o;
   const int ublk = d8.ublk;
   const int step8 = NL / 8;
@@ -334,28 +330,28 @@ __device__ __forceinline__ void gj_fill_dft8_dense(const FusedSrc& src, uint32_t
 // UC/MSC/NC: compile-time dense-fill geometry (0 = from g), see gj_fill_dft8_dense
 template <int UC = 0, int MSC = 0, int NC = 0>
 __device__ __forceinline__ void gj_fill_dft8(const FusedSrc& src, uint32_t* mats, const GjGeom& g, const int32_t* ids,
-                                             int64_t it, int64_t node_lo, uint32_t one, bool dense) {
+                                             const GjD8& d8, uint32_t one, bool dense) {
   if (dense) {
     switch (src.E) {
-      case 1: gj_fill_dft8_dense<1, UC, MSC, NC>(src, mats, g, it, node_lo); return;
-      case 2: gj_fill_dft8_dense<2, UC, MSC, NC>(src, mats, g, it, node_lo); return;
-      case 3: gj_fill_dft8_dense<3, UC, MSC, NC>(src, mats, g, it, node_lo); return;
-      case 4: gj_fill_dft8_dense<4, UC, MSC, NC>(src, mats, g, it, node_lo); return;
-      case 5: gj_fill_dft8_dense<5, UC, MSC, NC>(src, mats, g, it, node_lo); return;
-      case 6: gj_fill_dft8_dense<6, UC, MSC, NC>(src, mats, g, it, node_lo); return;
-      case 7: gj_fill_dft8_dense<7, UC, MSC, NC>(src, mats, g, it, node_lo); return;
-      default: gj_fill_dft8_dense<8, UC, MSC, NC>(src, mats, g, it, node_lo); return;
+      case 1: gj_fill_dft8_dense<1, UC, MSC, NC>(src, mats, g, d8); return;
+      case 2: gj_fill_dft8_dense<2, UC, MSC, NC>(src, mats, g, d8); return;
+      case 3: gj_fill_dft8_dense<3, UC, MSC, NC>(src, mats, g, d8); return;
+      case 4: gj_fill_dft8_dense<4, UC, MSC, NC>(src, mats, g, d8); return;
+      case 5: gj_fill_dft8_dense<5, UC, MSC, NC>(src, mats, g, d8); return;
+      case 6: gj_fill_dft8_dense<6, UC, MSC, NC>(src, mats, g, d8); return;
+      case 7: gj_fill_dft8_dense<7, UC, MSC, NC>(src, mats, g, d8); return;
+      default: gj_fill_dft8_dense<8, UC, MSC, NC>(src, mats, g, d8); return;
     }
   }
   switch (src.E) {
-    case 1: gj_fill_dft8_e<1>(src, mats, g, ids, it, node_lo, one); break;
-    case 2: gj_fill_dft8_e<2>(src, mats, g, ids, it, node_lo, one); break;
-    case 3: gj_fill_dft8_e<3>(src, mats, g, ids, it, node_lo, one); break;
-    case 4: gj_fill_dft8_e<4>(src, mats, g, ids, it, node_lo, one); break;
-    case 5: gj_fill_dft8_e<5>(src, mats, g, ids, it, node_lo, one); break;
-    case 6: gj_fill_dft8_e<6>(src, mats, g, ids, it, node_lo, one); break;
-    case 7: gj_fill_dft8_e<7>(src, mats, g, ids, it, node_lo, one); break;
-    default: gj_fill_dft8_e<8>(src, mats, g, ids, it, node_lo, one); break;
+    case 1: gj_fill_dft8_e<1>(src, mats, g, ids, d8, one); break;
+    case 2: gj_fill_dft8_e<2>(src, mats, g, ids, d8, one); break;
+    case 3: gj_fill_dft8_e<3>(src, mats, g, ids, d8, one); break;
+    case 4: gj_fill_dft8_e<4>(src, mats, g, ids, d8, one); break;
+    case 5: gj_fill_dft8_e<5>(src, mats, g, ids, d8, one); break;
+    case 6: gj_fill_dft8_e<6>(src, mats, g, ids, d8, one); break;
+    case 7: gj_fill_dft8_e<7>(src, mats, g, ids, d8, one); break;
+    default: gj_fill_dft8_e<8>(src, mats, g, ids, d8, one); break;
   }
 }
 
@@ -614,19 +610,21 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
 
   for (int64_t it = blockIdx.x; it < iters; it += gridDim.x) {
     __syncthreads();
+    GjD8 d8{};
     if constexpr (DFT8) {
+      d8 = gj_d8(src, g.U, it);
       if (PDB_GJ_ABL != 3 || it == blockIdx.x) {
         if constexpr (RPC > 0)   // launched with 256 threads, M = 256 / LPM matrices, RP = RPC
-          gj_fill_dft8<256 / LPM / 8, gj_matrix_stride(RPC, gj_row_stride(RPC)), RPC * RPC>(src, mats, g, ids, it,
-                                                                                           node_lo, one, dense);
+          gj_fill_dft8<256 / LPM / 8, gj_matrix_stride(RPC, gj_row_stride(RPC)), RPC * RPC>(src, mats, g, ids, d8,
+                                                                                           one, dense);
         else
-          gj_fill_dft8(src, mats, g, ids, it, node_lo, one, dense);
+          gj_fill_dft8(src, mats, g, ids, d8, one, dense);
       }
     }
     else gj_fill(src, mats, g, ids, it, node_lo, nodes, one, dense);
     __syncthreads();
     int64_t node;
-    if constexpr (DFT8) node = gj_node_dft8(src, it, slot, g);
+    if constexpr (DFT8) node = gj_node_dft8(src, d8, slot, g);
     else node = gj_node_linear(it, slot, g, nodes);
     if (node < 0) continue;
 

@@ -102,20 +102,23 @@ struct NodeMap {
   int64_t klen[PDB_MAP_DIMS] = {};       // compact extent per axis
   int64_t n8[PDB_MAP_DIMS] = {};         // N_a / 8
   int64_t stride[PDB_MAP_DIMS] = {};     // row-major stride of axis a in the full grid
+  int32_t small = 0;                     // full grid < 2^32 nodes: 32-bit index arithmetic
   __host__ __device__ __forceinline__ int64_t full(int64_t c) const {
     if (nd == 0) return c;
-    int64_t off = 0;
-    if (c < (1ll << 32)) {   // 32-bit div/mod on the common path
-      uint32_t cc = (uint32_t)c;
-      for (int a = nd - 1; a >= 0; --a) {
-        const uint32_t kl = (uint32_t)klen[a];
-        const uint32_t k = cc % kl;
-        cc /= kl;
-        const int64_t ax = u[a] ? (int64_t)(k % (uint32_t)u[a]) + n8[a] * (k / (uint32_t)u[a]) : (int64_t)k;
-        off += ax * stride[a];
-      }
-      return off;
+    if (!small) return full_big(c);
+    uint32_t cc = (uint32_t)c, off = 0;
+    for (int a = nd - 1; a >= 0; --a) {
+      const uint32_t kl = (uint32_t)klen[a];
+      const uint32_t k = cc % kl;
+      cc /= kl;
+      const uint32_t ax = u[a] ? k % (uint32_t)u[a] + (uint32_t)n8[a] * (k / (uint32_t)u[a]) : k;
+      off += ax * (uint32_t)stride[a];
     }
+    return off;
+  }
+  // grids of 2^32 nodes or more (out of line: 64-bit division)
+  __host__ __device__ __noinline__ int64_t full_big(int64_t c) const {
+    int64_t off = 0;
     for (int a = nd - 1; a >= 0; --a) {
       const int64_t k = c % klen[a];
       c /= klen[a];
@@ -156,6 +159,8 @@ struct FusedSrc {
   uint32_t p;
   NodeMap map;
   int ulast = 0;         // kept u of the last axis (NL / 8 when it is not pruned)
+  int64_t orow0 = 0;     // the launch's first compact last-axis row (node_lo / (8 ulast))
+  const int64_t* orow_full = nullptr;   // pruned map: full outer index of launch row j (det scratch)
   __device__ __forceinline__ int64_t node(int64_t c) const { return map.full(c); }
   __device__ __forceinline__ uint32_t at(int e, int64_t node) const {
     int64_t o = node / NL;

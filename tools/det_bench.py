@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--r", default="4,16,40")
     ap.add_argument("--nodes", type=int, default=1 << 20)
     ap.add_argument("--fused", action="store_true")
+    ap.add_argument("--pruned", action="store_true", help="profile only the pruned fused launch")
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
     out = {}
@@ -54,18 +55,27 @@ def main():
         out["staged_r%d" % r] = {"nodes": n, "s": t, "dets_per_s": n / t, "gupd_per_s": n * W / t / 1e9,
                                  "bytes_per_s": 4.0 * (r * r + 1) * n / t}
         del grids
-    if args.fused:
+    if args.fused or args.pruned:
         m, cfg = workloads.c5()
         pl = plan(m, cfg)
         st = executor.PrimeStages(m, pl, staged=False)
         st.forward(0)
         n = min(args.nodes, pl.node_count)
         dp = st.dp
+        st.scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, max(n, st.chunk)))
         c = st.ctx(0)
-        t = timed(lambda: native.eval_det_fused(c, st.work, dp.outer, dp.E, dp.k, pl.shape[-1], dp.ids, pl.r, 0, n,
-                                                st.det[:n], st.scratch), args.reps)
         W = (40 ** 3 - 40) // 3
-        out["fused_c5"] = {"nodes": n, "s": t, "dets_per_s": n / t, "gupd_per_s": n * W / t / 1e9}
+        if args.fused:
+            t = timed(lambda: native.eval_det_fused(c, st.work, dp.outer, dp.E, dp.k, pl.shape[-1], dp.ids, pl.r, 0,
+                                                    n, st.det[:n], st.scratch), args.reps)
+            out["fused_c5"] = {"nodes": n, "s": t, "dets_per_s": n / t, "gupd_per_s": n * W / t / 1e9}
+        if dp.nmap is not None:   # the same kernel over the kept (pruned) node set
+            row = dp.klen[-1]
+            npr = max(row, min(args.nodes, dp.sel) // row * row)
+            t = timed(lambda: native.eval_det_fused_map(c, st.work, dp.outer, dp.E, dp.k, pl.shape[-1], dp.ids,
+                                                        pl.r, dp.nmap, 0, npr, st.compact[:npr], st.scratch),
+                      args.reps)
+            out["fused_c5_pruned"] = {"nodes": npr, "s": t, "dets_per_s": npr / t, "gupd_per_s": npr * W / t / 1e9}
         tf = timed(lambda: st.forward(0), args.reps)
         ti = timed(lambda: st.interpolate(0), args.reps)
         out["c5_forward_s"] = tf
