@@ -136,17 +136,19 @@ __global__ void ntt_stage_global(uint32_t* __restrict__ data, AxisGeom g, int N,
 }
 
 // ---- sparse forward axis: input nonzero only on rows j < E <= 8 ------------
-// out[k] = sum_{j<E} x_j w^(jk) for every k = u + (N/8) v: the E input rows of
-// a tile of TI inner indices are staged in shared memory (every writer of
-// rows < E is in this CTA), then each thread evaluates 8 outputs of one
-// (u, t) by a twisted 8-point DFT.  Reads E/N of the axis instead of all of
-// it and does ~(E + 4)/8 mul-mods per output instead of log2(N)/2.  The
-// entries' coefficient boxes make this the common case of forward passes.
-template <int E>
+// out[k] = sum_{j<E} x_j w^(jk) for every k = u + (N/8) v: each thread owns V
+// consecutive inner columns (V = 4: 16-byte loads of the E input rows and
+// 16-byte stores of the outputs) and evaluates 8 outputs per column and u by
+// a twisted 8-point DFT.  Reads E/N of the axis instead of all of it and does
+// ~(E + 4)/8 mul-mods per output instead of log2(N)/2.  The entries'
+// coefficient boxes make this the common case of forward passes.  A CTA's
+// threads split the N/8 values of u of one tile of TI columns; the E rows are
+// read before any output of the tile is written (all writers of rows < E of
+// these columns are in this CTA, __syncthreads in between).
+template <int E, int V>
 __global__ void __launch_bounds__(256)
 ntt_axis_sparse(uint32_t* __restrict__ data, AxisGeom g, int N, int TI, const uint32_t* __restrict__ full,
                 const uint32_t* __restrict__ fulls, uint32_t p) {
-  __shared__ uint32_t xs[E * 32];
   const int N8 = N / 8;
   const int64_t tchunks = (g.inner + TI - 1) / TI;
   const int64_t ntiles = g.active_outer * tchunks;
@@ -154,23 +156,28 @@ ntt_axis_sparse(uint32_t* __restrict__ data, AxisGeom g, int N, int TI, const ui
   w[0] = ws[0] = 0;
 #pragma unroll
   for (int v = 1; v < 4; ++v) { w[v] = __ldg(full + v * N8); ws[v] = __ldg(fulls + v * N8); }
-  const int t = threadIdx.x % TI;
-  const int ug = threadIdx.x / TI, ugs = blockDim.x / TI;
+  const int cols = TI / V;                       // column groups per tile
+  const int cg = threadIdx.x % cols;
+  const int ug = threadIdx.x / cols, ugs = blockDim.x / cols;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t oc = tile / tchunks;
-    const int64_t t0 = (tile - oc * tchunks) * TI;
+    const int64_t t0 = (tile - oc * tchunks) * TI + (int64_t)cg * V;
     const int64_t base = outer_offset(oc, g) * (int64_t)N * g.inner + t0;
-    const bool live = t0 + t < g.inner;
-    __syncthreads();
-    for (int w2 = threadIdx.x; w2 < E * TI; w2 += blockDim.x) {
-      const int j = w2 / TI, tt = w2 - (w2 / TI) * TI;
-      xs[j * TI + tt] = t0 + tt < g.inner ? data[base + (int64_t)j * g.inner + tt] : 0u;
-    }
-    __syncthreads();
-    if (live && ug < ugs) {
-      uint32_t c[E];
+    const bool live = t0 < g.inner && ug < ugs;   // V | inner on the vector path
+    uint32_t c[V][E];
+    if (live) {
 #pragma unroll
-      for (int j = 0; j < E; ++j) c[j] = xs[j * TI + t];
+      for (int j = 0; j < E; ++j) {
+        if constexpr (V == 4) {
+          const uint4 q = *reinterpret_cast<const uint4*>(data + base + (int64_t)j * g.inner);
+          c[0][j] = q.x; c[1][j] = q.y; c[2][j] = q.z; c[3][j] = q.w;
+        } else {
+          c[0][j] = data[base + (int64_t)j * g.inner];
+        }
+      }
+    }
+    __syncthreads();   // every read of rows < E precedes every write
+    if (live) {
       for (int u = ug; u < N8; u += ugs) {
         uint32_t tw[8], tws[8];
         int kk = 0;
@@ -180,12 +187,18 @@ ntt_axis_sparse(uint32_t* __restrict__ data, AxisGeom g, int N, int TI, const ui
           else { tw[l] = tws[l] = 0; }
           kk += u;
         }
-        uint32_t x[8];
-        gj_dft8<E>(c, tw, tws, w, ws, p, x);
+        uint32_t x[V][8];
 #pragma unroll
-        for (int v = 0; v < 8; ++v) data[base + (int64_t)(u + v * N8) * g.inner + t] = x[v];
+        for (int q = 0; q < V; ++q) gj_dft8<E>(c[q], tw, tws, w, ws, p, x[q]);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          uint32_t* o = data + base + (int64_t)(u + v * N8) * g.inner;
+          if constexpr (V == 4) *reinterpret_cast<uint4*>(o) = make_uint4(x[0][v], x[1][v], x[2][v], x[3][v]);
+          else *o = x[0][v];
+        }
       }
     }
+    __syncthreads();
   }
 }
 
@@ -214,14 +227,23 @@ int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t
   const int logN = 31 - __builtin_clz((unsigned)N);
   const int64_t E = ext ? ext[axis] : N;
   if (!inverse && E >= 1 && E <= 8 && N >= 16 && !getenv("PDB_NTT_DENSE")) {
-    // the input is nonzero only on rows < E of this axis: evaluate, don't transform
-    const int TI = (int)(g.inner < 32 ? g.inner : 32);
-    const int threads = (256 / TI) * TI;
+    // the input is nonzero only on rows < E of this axis: evaluate, don't transform.
+    // Tiles of TI inner columns, V = 4 columns per thread when the rows allow 16-byte access.
+    const bool vec = g.inner % 4 == 0 && (reinterpret_cast<uintptr_t>(data) & 15) == 0;
+    const int V = vec ? 4 : 1;
+    int TI = (int)(g.inner < 32 * V ? g.inner : 32 * V);
+    if (vec) TI &= ~3;
+    const int cols = TI / V;
+    int ugs = 256 / cols;                       // u-groups per CTA: at most N/8
+    if (ugs > N / 8) ugs = N / 8;
+    const int threads = ugs * cols;
     const int64_t tiles = g.active_outer * ((g.inner + TI - 1) / TI);
     const int grid = (int)(tiles < (int64_t)ctx->sms * 16 ? tiles : (int64_t)ctx->sms * 16);
     const uint32_t p = (uint32_t)ctx->p;
-    switch (E) {
-#define PDB_SPARSE(EE) case EE: ntt_axis_sparse<EE><<<grid, threads, 0, st>>>(data, g, N, TI, T->full, T->full_s, p); break;
+    switch (E * 2 + (vec ? 1 : 0)) {
+#define PDB_SPARSE(EE)                                                                                        \
+  case EE * 2: ntt_axis_sparse<EE, 1><<<grid, threads, 0, st>>>(data, g, N, TI, T->full, T->full_s, p); break; \
+  case EE * 2 + 1: ntt_axis_sparse<EE, 4><<<grid, threads, 0, st>>>(data, g, N, TI, T->full, T->full_s, p); break;
       PDB_SPARSE(1) PDB_SPARSE(2) PDB_SPARSE(3) PDB_SPARSE(4)
       PDB_SPARSE(5) PDB_SPARSE(6) PDB_SPARSE(7) PDB_SPARSE(8)
 #undef PDB_SPARSE

@@ -440,12 +440,18 @@ def _expand(dp: DevicePlan, ctx, compact, grid):
         native.grid_expand(ctx, compact, grid, dp.nmap)
 
 
-def _sparse_leading_axes(dp: DevicePlan) -> bool:
-    """True when ntt.cu evaluates every fused-mode leading axis with the sparse
-    kernel (forward, <= 8 nonzero rows, length >= 16; or length 1)."""
+def _sparse_axes(shape, ext) -> bool:
+    """True when ntt.cu evaluates every one of these forward axes with the
+    sparse kernel (<= 8 nonzero rows, length >= 16; or length 1), which reads
+    only the coefficient box and writes every output position: then only the
+    box needs zeroing before the scatter, not the whole grid buffer."""
     if os.environ.get("PDB_NTT_DENSE"):
         return False
-    return all(n == 1 or (1 <= e <= 8 and n >= 16) for n, e in zip(dp.shape[:-1], dp.ext[:-1]))
+    return all(n == 1 or (1 <= e <= 8 and n >= 16) for n, e in zip(shape, ext))
+
+
+def _sparse_leading_axes(dp: DevicePlan) -> bool:
+    return _sparse_axes(dp.shape[:-1], dp.ext[:-1])
 
 
 def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
@@ -490,7 +496,11 @@ def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
                 native.reduce_scatter(ctx, dp.mag[lo:], dp.neg[lo:], dp.pos[lo:], hi - lo, dp.L, work)
             native.ntt_multi(ctx, sl, 1, dp.shape, dp.ext, range(dp.vn), False)
     else:
-        work.zero_()
+        if dp.vn and _sparse_axes(dp.shape, dp.ext):
+            box = work[: dp.k * dp.nodes].view((dp.k,) + dp.shape)[(slice(None),) + tuple(slice(0, e) for e in dp.ext)]
+            box.zero_()
+        else:
+            work.zero_()
         native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, work)
         native.ntt_multi(ctx, work, dp.k, dp.shape, dp.ext, range(dp.vn), False)
     for eid in todo:
