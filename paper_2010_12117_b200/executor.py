@@ -496,7 +496,7 @@ def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
                 native.reduce_scatter(ctx, dp.mag[lo:], dp.neg[lo:], dp.pos[lo:], hi - lo, dp.L, work)
             native.ntt_multi(ctx, sl, 1, dp.shape, dp.ext, range(dp.vn), False)
     else:
-        if dp.vn and _sparse_axes(dp.shape, dp.ext):
+        if dp.vn and not dp.wide and _sparse_axes(dp.shape, dp.ext):   # (the u64 NTT is dense)
             box = work[: dp.k * dp.nodes].view((dp.k,) + dp.shape)[(slice(None),) + tuple(slice(0, e) for e in dp.ext)]
             box.zero_()
         else:
