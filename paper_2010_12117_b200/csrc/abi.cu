@@ -161,6 +161,7 @@ static bool make_node_map(const pdb_node_map* in, NodeMap* out, int64_t* size) {
     stride *= N;
     n *= out->klen[a];
   }
+  out->small = stride < (1ll << 32);
   *size = n;
   return true;
 }
@@ -367,6 +368,7 @@ int32_t pdb_eval_det_fused_u32(pdb_prime_ctx* ctx, const uint32_t* partial, int6
   if (!T) return -2;
   FusedSrc src{partial, outer, ncoef, entries, n_last, T->full, T->full_s, ctx->m.p};
   src.ulast = n_last / 8;
+  if (src.ulast > 0) src.orow0 = node_lo / (8 * (int64_t)src.ulast);
   return det_run(ctx, src, entry_ids, r, node_lo, nodes, out, scratch, scratch_bytes, (cudaStream_t)stream);
 }
 
@@ -417,6 +419,7 @@ int32_t pdb_eval_det_fused_map_u32(pdb_prime_ctx* ctx, const uint32_t* partial, 
     if (node_lo < 0 || node_lo + nodes > n) { set_error("node range outside the node map"); return -2; }
     if (src.map.u[map->ndim - 1]) src.ulast = src.map.u[map->ndim - 1];
   }
+  if (src.ulast > 0) src.orow0 = node_lo / (8 * (int64_t)src.ulast);
   return det_run(ctx, src, entry_ids, r, node_lo, nodes, out, scratch, scratch_bytes, (cudaStream_t)stream);
 }
 

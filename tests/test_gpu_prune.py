@@ -122,3 +122,17 @@ def test_node_map_validation(cuda):
         native.node_map_size(native.node_map((64, 32), (8, 3)))    # 8 U = N
     with pytest.raises(ValueError):
         native.node_map_size(native.node_map((48, 32), (2, 3)))    # not a power of two
+
+
+@pytest.mark.parametrize("prune", [False, True])
+@pytest.mark.parametrize("r,vn,degs,seed", [(10, 2, (4, 4), 2), (40, 2, (2, 2), 7), (10, 3, (2, 4, 3), 5)])
+def test_fused_multi_launch_equals_staged(cuda, monkeypatch, prune, r, vn, degs, seed):
+    """The fused determinant runs in chunks of whole last-axis rows; with a tiny
+    chunk every launch starts mid-grid (the per-launch row offset, the pruned
+    row table).  Its grid must equal the staged computation's."""
+    m = _dense(r, vn, degs, seed)
+    staged, _ = _grids(m, "staged", False, primes=(0,))
+    monkeypatch.setattr(executor, "FUSED_CHUNK", 512)
+    fused, dp = _grids(m, "fused", prune, primes=(0,))
+    assert dp.sel // executor.det_chunk_size(dp) >= 2
+    assert np.array_equal(staged[0], fused[0])
