@@ -394,6 +394,7 @@ def run_ours(args):
     ws_bytes = working_set_bytes(m, pl)
     flush = None if ws_bytes > 2 * L2_BYTES else torch.empty(64 * 2**20, dtype=torch.int32, device=dev)
     step_events = []
+    native.kernel_timing(True)   # CUDA events around every det_gj launch, on its launch stream
     for s in range(args.steps):
         pi = prime_of(s)
         if flush is not None:
@@ -414,6 +415,8 @@ def run_ours(args):
         step_events.append((t0, t1))
     barrier()
     clocks = sampler.stop()
+    kern_ms, kern_launches = native.kernel_timing_read()
+    native.kernel_timing(False)
     launches = native.launch_count() - launches0
     ms = sum(a.elapsed_time(b) for a, b in step_events)
     det_ms = sum(a.elapsed_time(b) for a, b in det_events)
@@ -484,7 +487,9 @@ def run_ours(args):
 
     r = m.r
     W = (r ** 3 - r) // 3
-    achieved = W * sel * args.steps / (det_ms / 1e3)
+    # the roofline's kernel: det_gj launches alone (device time from the events
+    # around each launch); det_ms adds the finalize and row-table launches
+    achieved = W * sel * args.steps / (kern_ms / 1e3)
     hbm, hbm_kind = measured_peaks()
     launch_nodes = chunk
     traffic = traffic_note = ncu_summary = None
@@ -515,7 +520,7 @@ def run_ours(args):
         "roofline": {"bound": "int", "kernel": "det_gj_kernel<FusedSrc> (eval + elimination)",
                      "achieved": achieved / 1e9, "peak": peak_delayed / 1e9, "unit": "Gupd/s",
                      "frac": achieved / peak_delayed, "traffic": traffic, "traffic_note": traffic_note,
-                     "hbm_achieved_gbs": (traffic / launch_nodes) * sel * args.steps / (det_ms / 1e3) / 1e9
+                     "hbm_achieved_gbs": (traffic / launch_nodes) * sel * args.steps / (kern_ms / 1e3) / 1e9
                      if traffic else None,
                      "peak_kind": "measured now: 9 MACs + one REDC, the trailing-update primitive "
                                   "(pdb_mulmod_peak variant 1)",
@@ -523,7 +528,12 @@ def run_ours(args):
                      "frac_vs_imadwide_ceiling": achieved / peak_imadwide,
                      "imadwide_note": "raw accumulating IMAD.WIDE stream measured now (variant 2): the integer "
                                       "multiplier's ceiling if every update were one bare MAC",
+                     "kernel_ms_per_step": kern_ms / args.steps, "kernel_launches_per_step": kern_launches / args.steps,
+                     "kernel_share": kern_ms / ms,
+                     "kernel_timing": "CUDA events recorded by the library around every det_gj launch on its launch "
+                                      "stream (pdb_kernel_timing), summed over the timed steps",
                      "det_ms_per_step": det_ms / args.steps, "det_share": det_ms / ms,
+                     "frac_det_stage": W * sel * args.steps / (det_ms / 1e3) / peak_delayed,
                      "work_per_matrix": W, "hbm_peak_gbs": hbm, "hbm_peak_kind": hbm_kind,
                      "ncu": ncu_summary},
         "clocks": clocks,

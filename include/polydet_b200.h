@@ -158,6 +158,13 @@ int32_t pdb_crt_mrc_sel_u32(const uint32_t* residues, int32_t nprimes, int64_t s
  * IMAD.WIDE stream (the integer multiplier's ceiling, MACs/s). */
 int32_t pdb_mulmod_peak(uint32_t p, int32_t variant, double* updates_per_second, void* stream);
 
+/* Profiling hook (no reference counterpart): while enabled, every det_gj kernel
+ * launch is bracketed by CUDA events on its launch stream.  pdb_kernel_timing
+ * enables (1) or disables (0) it and clears the record; pdb_kernel_timing_read
+ * waits for the recorded launches and returns their summed device time. */
+int32_t pdb_kernel_timing(int32_t enable);
+int32_t pdb_kernel_timing_read(double* ms, int64_t* launches);
+
 /* ---- the wide path: primes 2^31 <= p < 2^62 --------------
  * u64 twins of the entry points above for contexts created with p >= 2^31
  * (reference object/int64 dtype paths, tensor.py:152-154).  Residues are u64;

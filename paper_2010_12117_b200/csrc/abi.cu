@@ -1,5 +1,6 @@
 // extern "C" boundary of libpolydet_b200.so (declared in include/polydet_b200.h).
 #include <atomic>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <vector>
@@ -16,6 +17,32 @@ static thread_local char g_err[512] = "";
 static std::atomic<long long> g_launches{0};
 
 void count_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ---- det kernel timing (pdb_kernel_timing): event pairs around det_gj launches ----
+static std::mutex g_kt_lock;
+static bool g_kt_on = false;
+static std::vector<cudaEvent_t> g_kt_events;   // start, stop, start, stop, ...
+static size_t g_kt_used = 0;
+
+int ktimer_start(cudaStream_t st) {
+  std::lock_guard<std::mutex> guard(g_kt_lock);
+  if (!g_kt_on) return -1;
+  while (g_kt_events.size() < g_kt_used + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    g_kt_events.push_back(e);
+  }
+  const int slot = (int)g_kt_used;
+  g_kt_used += 2;
+  cudaEventRecord(g_kt_events[slot], st);
+  return slot;
+}
+
+void ktimer_stop(int slot, cudaStream_t st) {
+  if (slot < 0) return;
+  std::lock_guard<std::mutex> guard(g_kt_lock);
+  cudaEventRecord(g_kt_events[slot + 1], st);
+}
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -472,6 +499,28 @@ int32_t pdb_crt_mrc_sel_u32(const uint32_t* residues, int32_t nprimes, int64_t s
   int sms = pdb_device_sm_count(dev);
   return crt_mrc_sel(residues, nprimes, index, count, stride, primes, limbs, L, neg, width, sms > 0 ? sms : 148,
                      (cudaStream_t)stream);
+}
+
+int32_t pdb_kernel_timing(int32_t enable) {
+  std::lock_guard<std::mutex> guard(g_kt_lock);
+  g_kt_on = enable != 0;
+  g_kt_used = 0;
+  return 0;
+}
+
+int32_t pdb_kernel_timing_read(double* ms, int64_t* launches) {
+  if (!ms || !launches) { set_error("null output pointer"); return -2; }
+  std::lock_guard<std::mutex> guard(g_kt_lock);
+  double total = 0;
+  for (size_t i = 0; i + 1 < g_kt_used; i += 2) {
+    if (cudaEventSynchronize(g_kt_events[i + 1]) != cudaSuccess) return check_launch("kernel timing");
+    float t = 0;
+    cudaEventElapsedTime(&t, g_kt_events[i], g_kt_events[i + 1]);
+    total += t;
+  }
+  *ms = total;
+  *launches = (int64_t)(g_kt_used / 2);
+  return 0;
 }
 
 int32_t pdb_mulmod_peak(uint32_t p, int32_t variant, double* ups, void* stream) {

@@ -298,14 +298,18 @@ static int launch_gj_geom(PrimeCtx* ctx, const GjGeom& g, Src src, const int32_t
   const int threads = g.M * LPM;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, det_gj_kernel<Src, DFT8, LPM, P31, RPC>, threads, smem);
   if (ctas_per_sm < 1) ctas_per_sm = 1;
+  static const char* cenv = getenv("PDB_GJ_CTAS");   // experiments: cap resident CTAs per SM
+  if (cenv && *cenv && atoi(cenv) > 0 && atoi(cenv) < ctas_per_sm) ctas_per_sm = atoi(cenv);
   const int64_t iters = DFT8 ? nodes / g.M : (nodes + g.M - 1) / g.M;
   const int64_t cap = (int64_t)ctx->sms * ctas_per_sm;
   const int grid = (int)(iters < cap ? iters : cap);
   if (grid < 1) return 0;
+  const int kt = ktimer_start(st);
   det_gj_kernel<Src, DFT8, LPM, P31, RPC><<<grid, threads, smem, st>>>(src, ids, node_lo, nodes, out, den, fc, fn, g, ctx->m);
+  ktimer_stop(kt, st);
   count_launch();
   if (int rc = check_launch("det_gj")) return rc;
-  const int64_t fblocks = (nodes + 255) / 256;
+  const int64_t fblocks = (nodes + 256 * GJ_FIN_D - 1) / (256 * GJ_FIN_D);
   const int fgrid = (int)(fblocks < (int64_t)ctx->sms * 8 ? fblocks : (int64_t)ctx->sms * 8);
   det_gj_finalize<<<fgrid, 256, 0, st>>>(out, den, nodes, mont_scale(ctx->m, g.r), ctx->m);
   count_launch();

@@ -61,6 +61,16 @@ __host__ __device__ constexpr int gj_matrix_stride(int RP, int S) {
   return RP * S + GJ_NX_WORDS + ((16 - (RP * S + GJ_NX_WORDS) % 32) + 32) % 32;
 }
 
+#define PDB_PRAGMA_(x) _Pragma(#x)
+#define PDB_UNROLL_(n) PDB_PRAGMA_(unroll n)
+#define PDB_UNROLL(n) PDB_UNROLL_(n)
+#ifndef PDB_GJ_TUNROLL
+#define PDB_GJ_TUNROLL 2   // unroll factor of the trailing-update tile loop (measured: 2 +1.4 %, 3, 4, 8 -12 %)
+#endif
+#ifndef PDB_GJ_MUNROLL
+#define PDB_GJ_MUNROLL 1   // unroll factor of the M-pass item loop
+#endif
+
 #ifndef PDB_GJ_MINB
 #define PDB_GJ_MINB 2   // resident 256-thread CTAs per SM the register budget is sized for
 #endif
@@ -80,14 +90,21 @@ struct GjGeom {
 
 __host__ __device__ constexpr int gj_row_stride(int RP) { return RP + PDB_GJ_ROWPAD; }
 
+#ifndef PDB_REDC_ADD
+#define PDB_REDC_ADD 0   // 1: additive REDC form (ptxas still emits IMAD.HI; measured 1.8 % slower)
+#endif
+__device__ __forceinline__ uint32_t gj_redc(uint64_t acc, const Mod32& m) {
+  return PDB_REDC_ADD ? redc_add(acc, m) : redc(acc, m);
+}
+
 // REDC of a <= 9-product accumulator, canonical: two conditional subtractions.
 __device__ __forceinline__ uint32_t gj_red(uint64_t acc, const Mod32& m) {
-  const uint32_t v = redc(acc, m);
+  const uint32_t v = gj_redc(acc, m);
   return csub(csub(v, 2u * m.p), m.p);
 }
 
 // REDC of <= 2 products of canonical residues: output < 1.5 p, one subtraction.
-__device__ __forceinline__ uint32_t gj_red2(uint64_t acc, const Mod32& m) { return csub(redc(acc, m), m.p); }
+__device__ __forceinline__ uint32_t gj_red2(uint64_t acc, const Mod32& m) { return csub(gj_redc(acc, m), m.p); }
 
 // Montgomery product of canonical a, b (Montgomery forms stay Montgomery forms).
 __device__ __forceinline__ uint32_t gj_mont(uint32_t a, uint32_t b, const Mod32& m) {
@@ -417,6 +434,7 @@ __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, ui
   const uint32_t* npr = A + K * S;    // negM rows K..K+7
   int ti = l / ntc, tc = l - (l / ntc) * ntc;
   const int dti = LPM / ntc, dtc = LPM - (LPM / ntc) * ntc;
+  PDB_UNROLL(PDB_GJ_TUNROLL)
   for (int w = l; w < tiles; w += LPM) {
     const int i0 = c0 + TR * ti, cc = c0 + TC * tc;
     // 8-wide tiles: odd tile rows visit their two 16-byte chunks in swapped order,
@@ -498,6 +516,7 @@ __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S,
                                          unsigned omask, const Mod32& m) {
   constexpr int NRG = B / RPI;
   const int items = (mrem / TC) * NRG;
+  PDB_UNROLL(PDB_GJ_MUNROLL)
   for (int w0 = 0; w0 < items; w0 += LPM) {
     const int w = w0 + l;
     const bool act = w < items;
@@ -559,6 +578,12 @@ __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, in
 }
 
 // ---- the kernel ------------------------------------------------------------------------------
+#ifndef PDB_GJ_GELAST
+#define PDB_GJ_GELAST 1   // last pivot block: elimination without the Gauss-Jordan back part
+#endif
+#ifndef PDB_GJ_DS
+#define PDB_GJ_DS 0   // 1: pivot pairs by 2x2 Cramer steps (measured ~1 % slower than one pivot per step)
+#endif
 #ifndef PDB_GJ_ABL
 #define PDB_GJ_ABL 0   // profiling ablation only (1: no M pass, 2: no T pass, 3: one fill per CTA); results are wrong
 #endif
@@ -647,14 +672,109 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
 #pragma unroll
         for (int k = 0; k < EPL; ++k) v[k] = src_row[k];
       }
+      if constexpr (PDB_GJ_DS && !P31 && EPL >= 2 && B % 2 == 0) {
+        // Pivot pairs (s, s+1) eliminated at once by the 2x2 Cramer step, all in
+        // the augmented [A11 | E] stored in place (E column s enters as sigma e_s):
+        //   pivot block P = [[a, b], [c, d]], D = det P, sigma = D_0 ... D_{k-1};
+        //   other rows  R_i <- D R_i - alpha_i R_s - beta_i R_{s+1},
+        //               alpha_i = d t_a - c t_b, beta_i = a t_b - b t_a  (t = row i at s, s+1);
+        //   pivot rows  [R_s; R_{s+1}] <- sigma adj(P) [R_s; R_{s+1}].
+        // Every row keeps the common scale sigma, so after B/2 steps the A11 part is
+        // c I with c = prod D_k and the E part is X = c A11^-1 (same contract as
+        // the single-step elimination below); det A11 = prod D_k / prod sigma_k^2.
+        // Per pair: 3 products + one REDC per element (two single steps: 4 + 2).
+        uint32_t sig = one, sprod = one;
+#pragma unroll
+        for (int kp = 0; kp < B / 2; ++kp) {
+          const int s = 2 * kp;
+          const int ks = s % EPL, ls = s / EPL;   // element index / lane-in-row of columns s, s+1
+          const uint32_t a = __shfl_sync(omask, v[ks], s * LPR + ls, LPM);
+          const uint32_t b = __shfl_sync(omask, v[ks + 1], s * LPR + ls, LPM);
+          const uint32_t c = __shfl_sync(omask, v[ks], (s + 1) * LPR + ls, LPM);
+          const uint32_t d = __shfl_sync(omask, v[ks + 1], (s + 1) * LPR + ls, LPM);
+          const uint32_t D = gj_red2(mad_wide(a, d, mad_wide(p - b, c, 0ull)), m);
+          if (kp >= 1) sprod = gj_mont(sprod, sig, m);
+          if (mrem == 0 && kp == B / 2 - 1) {   // last block, last pair: only its D is needed
+            sig = gj_mont(sig, D, m);
+            break;
+          }
+          const uint32_t ta = __shfl_sync(omask, v[ks], pj * LPR + ls, LPM);
+          const uint32_t tb = __shfl_sync(omask, v[ks + 1], pj * LPR + ls, LPM);
+          const bool ps_row = pj == s, ps1_row = pj == s + 1, piv = ps_row || ps1_row;
+          // this lane's half of the row coefficients: nu (even lanes) or rho (odd lanes)
+          uint32_t cf[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (LPR >= 2 && h != ((l % LPR) & 1)) continue;
+            uint32_t m1, n1, m2, n2;
+            if (h == 0) { m1 = piv ? sig : c; n1 = ps_row ? d : (ps1_row ? p - c : tb); m2 = piv ? 0u : p - d; n2 = ta; }
+            else { m1 = piv ? sig : b; n1 = ps_row ? p - b : (ps1_row ? a : ta); m2 = piv ? 0u : p - a; n2 = tb; }
+            cf[h] = gj_red2(mad_wide(m1, n1, mad_wide(m2, n2, 0ull)), m);
+          }
+          uint32_t nu, rho;
+          if constexpr (LPR >= 2) {
+            const bool odd = (l % LPR) & 1;
+            const uint32_t mine = odd ? cf[1] : cf[0];
+            const uint32_t other = __shfl_xor_sync(omask, mine, 1, LPM);
+            nu = odd ? other : mine;
+            rho = odd ? mine : other;
+          } else {
+            nu = cf[0];
+            rho = cf[1];
+          }
+          const uint32_t mu = piv ? 0u : D;
+          const bool inj = (l % LPR) == ls;   // this lane holds columns s, s+1 (E columns enter here)
+#pragma unroll
+          for (int k = 0; k < EPL; ++k) {
+            // last block: only columns > s + 1 feed a later pivot (some lane's column pc + k)
+            if (mrem == 0 && !(B - EPL + k > s + 1)) continue;
+            uint32_t x = v[k];
+            uint32_t y = __shfl_sync(omask, v[k], s * LPR + l % LPR, LPM);
+            uint32_t z = __shfl_sync(omask, v[k], (s + 1) * LPR + l % LPR, LPM);
+            if (k == ks) {
+              x = inj ? (ps_row ? sig : 0u) : x;
+              y = inj ? sig : y;
+              z = inj ? 0u : z;
+            } else if (k == ks + 1) {
+              x = inj ? (ps1_row ? sig : 0u) : x;
+              y = inj ? 0u : y;
+              z = inj ? sig : z;
+            }
+            v[k] = gj_red2(mad_wide(mu, x, mad_wide(nu, y, mad_wide(rho, z, 0ull))), m);
+          }
+          sig = gj_mont(sig, D, m);
+        }
+        if (sig == 0) return false;   // some D_k vanished
+        // det(A11) = c / (sigma_1 ... sigma_{B/2-1})^2; one lane carries the factor
+        den = gj_mont(den, l == 0 ? gj_mont(sprod, sprod, m) : one, m);
+        num = gj_mont(num, sig, m);
+        if (mrem == 0) return true;
+        const uint32_t cR = sig;
+        Q = gj_mont(Q, cR, m);
+        if (K + B < RP - TAIL4) C8 = gj_mont(C8, Q, m);
+        else C4 = gj_mont(C4, Q, m);
+#pragma unroll
+        for (int k = 0; k < EPL; ++k) NX[gj_nx_row(pj) + pc + k] = v[k] ? p - v[k] : 0u;
+        __syncwarp(omask);
+        if (PDB_GJ_ABL != 1) gj_mpass_any<LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
+        __syncwarp(omask);
+        if (PDB_GJ_ABL != 2) gj_tpass_any<LPM, P31, B>(A, S, K, mrem, cR, l, m);
+        __syncwarp(omask);
+        return true;
+      }
       uint32_t lam = one, zl = one, zlast = one;
 #pragma unroll
       for (int s = 0; s < B; ++s) {
         const uint32_t z = __shfl_sync(omask, v[s % EPL], s * LPR + s / EPL, LPM);
         const uint32_t t = __shfl_sync(omask, v[s % EPL], pj * LPR + s / EPL, LPM);
+        // last block (no trailing rows): only det(A11) is needed, i.e. the pivots --
+        // Gaussian elimination suffices, and column slots k whose column is <= s in
+        // every lane of the group (B - EPL + k <= s) are dead from step s on
+        auto live = [&](int k) { return !(PDB_GJ_GELAST && mrem == 0) || B - EPL + k > s; };
         uint32_t prow[EPL];
 #pragma unroll
-        for (int k = 0; k < EPL; ++k) prow[k] = __shfl_sync(omask, v[k], s * LPR + l % LPR, LPM);
+        for (int k = 0; k < EPL; ++k)
+          if (live(k)) prow[k] = __shfl_sync(omask, v[k], s * LPR + l % LPR, LPM);
         // Other rows: z v - t prow, with -t lam at column s (the identity column of
         // row s is lam there).  Row s is scaled by lam = prod_{t<s} z_t instead
         // (lam * v; lam^2 at column s): then every row ends up scaled by c =
@@ -665,6 +785,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         const uint32_t nn = piv ? 0u : p - t;   // p - t in (0, p]: a valid 2-product multiplier
 #pragma unroll
         for (int k = 0; k < EPL; ++k) {
+          if (!live(k)) continue;
           uint32_t a = v[k], b = prow[k];
           if (k == s % EPL) {   // the only element of this lane that can sit in column s
             const bool diag = pc == s - s % EPL;
@@ -737,33 +858,49 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
   }
 }
 
-// det = num / den * R^r per node (Montgomery forms), 32 inversions per Fermat.
+// det = num / den * R^r per node (Montgomery forms).  Each lane owns D nodes
+// (lane-strided, coalesced); prefix products in the lane, then across the warp
+// by shuffles: one Fermat inversion per 32 D nodes (the exponentiation, not the
+// 12 bytes of traffic per node, bounded the one-node-per-lane version).
+constexpr int GJ_FIN_D = 8;
 __global__ void __launch_bounds__(256)
 det_gj_finalize(uint32_t* __restrict__ out, const uint32_t* __restrict__ den, int64_t nodes, uint32_t Rr, Mod32 m) {
+  constexpr int D = GJ_FIN_D;
   const int lane = threadIdx.x & 31;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < nodes; base += stride) {
-    const int64_t idx = base + lane;
-    const bool valid = idx < nodes;
-    const uint32_t d = valid ? den[idx] : 0u;
-    const bool use = d != 0u;
-    const uint32_t x = use ? d : m.r1;
-    uint32_t pre_x = x, suf_x = x;
+  const uint32_t one = m.r1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * D;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * D; base < nodes; base += stride) {
+    uint32_t dv[D], pre[D];
+    uint32_t run = one;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int64_t idx = base + d * 32 + lane;
+      dv[d] = idx < nodes ? den[idx] : 0u;
+      run = gj_mont(run, dv[d] ? dv[d] : one, m);   // flagged (0) and tail nodes count as 1
+      pre[d] = run;                                  // product of this lane's dens up to d
+    }
+    uint32_t pre_x = run, suf_x = run;
 #pragma unroll
     for (int k = 1; k < 32; k <<= 1) {
       const uint32_t up = __shfl_up_sync(0xffffffffu, pre_x, k);
       const uint32_t dn = __shfl_down_sync(0xffffffffu, suf_x, k);
-      if (lane >= k) pre_x = mont(pre_x, up, m);
-      if (lane + k < 32) suf_x = mont(suf_x, dn, m);
+      if (lane >= k) pre_x = gj_mont(pre_x, up, m);
+      if (lane + k < 32) suf_x = gj_mont(suf_x, dn, m);
     }
-    const uint32_t totalR = __shfl_sync(0xffffffffu, pre_x, 31);
-    const uint32_t inv_totalR = mont_pow(totalR, (uint64_t)m.p - 2, m);
+    const uint32_t total = __shfl_sync(0xffffffffu, pre_x, 31);
+    const uint32_t inv_total = mont_pow(total, (uint64_t)m.p - 2, m);
     uint32_t left = __shfl_up_sync(0xffffffffu, pre_x, 1);
     uint32_t right = __shfl_down_sync(0xffffffffu, suf_x, 1);
-    if (lane == 0) left = m.r1;
-    if (lane == 31) right = m.r1;
-    const uint32_t invR = mont(mont(left, right, m), inv_totalR, m);
-    if (use) out[idx] = mont(mont(out[idx], invR, m), Rr, m);
+    if (lane == 0) left = one;
+    if (lane == 31) right = one;
+    uint32_t inv = gj_mont(gj_mont(left, right, m), inv_total, m);   // 1 / (this lane's product)
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) {
+      const int64_t idx = base + d * 32 + lane;
+      const uint32_t inv_d = d ? gj_mont(inv, pre[d - 1], m) : inv;   // 1 / dv[d]
+      inv = gj_mont(inv, dv[d] ? dv[d] : one, m);
+      if (idx < nodes && dv[d]) out[idx] = gj_mont(gj_mont(out[idx], inv_d, m), Rr, m);
+    }
   }
 }
 

@@ -109,6 +109,22 @@ PDB_HD uint32_t redc(uint64_t acc, const Mod32& m) {
   return (uint32_t)(acc >> 32) + m.p - umulhi32(mq, m.p);
 }
 
+// The same reduction in additive form: with nq = -lo(acc) * p^-1 mod 2^32,
+// acc + nq*p == 0 (mod 2^32) and v = hi(acc + nq*p) = acc * 2^-32 (mod p),
+// v <= hi(acc) + p.  The 64-bit sum is one accumulating IMAD.WIDE (no IMAD.HI,
+// no IADD3); valid whenever acc + (2^32 - 1) p < 2^64 (e.g. 9 products of
+// residues for p < 2^30, 2 for p < 2^31).
+PDB_HD uint32_t redc_add(uint64_t acc, const Mod32& m) {
+  const uint32_t nq = (uint32_t)acc * (0u - m.qinv);
+#ifdef __CUDA_ARCH__
+  uint32_t lo = (uint32_t)acc, hi = (uint32_t)(acc >> 32);
+  asm("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.u32 %1, %2, %3, %1;" : "+r"(lo), "+r"(hi) : "r"(nq), "r"(m.p));
+  return hi;
+#else
+  return (uint32_t)((acc + (uint64_t)nq * m.p) >> 32);
+#endif
+}
+
 // Any 32-bit v -> [0, p).
 PDB_HD uint32_t canon32(uint32_t v, const Mod32& m) {
   uint32_t q = umulhi32(v, m.mu);

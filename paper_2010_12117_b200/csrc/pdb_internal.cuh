@@ -81,6 +81,10 @@ void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 // Counts kernel launches issued by this library (pdb_launch_count()).
 void count_launch(long long n = 1);
+// pdb_kernel_timing: CUDA events on the launch stream around a det_gj launch
+// (ktimer_start returns -1 while timing is off).
+int ktimer_start(cudaStream_t st);
+void ktimer_stop(int slot, cudaStream_t st);
 
 int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t* dims,
              const int64_t* ext, int axis, bool inverse, cudaStream_t st);

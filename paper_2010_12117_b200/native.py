@@ -75,6 +75,8 @@ _SIGNATURES = {
     "pdb_crt_mrc_sel_u32": (_c_i32, [_c_vp, _c_i32, _c_i64, _c_vp, _c_vp, _c_i64, _c_vp, _c_i32, _c_vp, _c_vp,
                                      _c_vp]),
     "pdb_mulmod_peak": (_c_i32, [_c_u32, _c_i32, ctypes.POINTER(ctypes.c_double), _c_vp]),
+    "pdb_kernel_timing": (_c_i32, [_c_i32]),
+    "pdb_kernel_timing_read": (_c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_c_i64)]),
     # the wide path (2^31 <= p < 2^62): u64 twins
     "pdb_prime_ctx_create_wide": (_c_i32, [_c_u64, _c_u64, _c_i32, ctypes.POINTER(_c_vp)]),
     "pdb_ntt_multi_u64": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp, _c_u32, _c_i32, _c_vp]),
@@ -360,6 +362,18 @@ def crt_mrc_sel(residues, nprimes: int, stride: int, primes, index, count: int, 
 def launch_count() -> int:
     """Kernels this process has launched through the library (all devices)."""
     return int(load_library().pdb_launch_count())
+
+
+def kernel_timing(enable: bool) -> None:
+    """Start (clearing the record) or stop CUDA-event timing of every det_gj launch."""
+    check(load_library().pdb_kernel_timing(1 if enable else 0), "kernel timing")
+
+
+def kernel_timing_read():
+    """(summed device ms, launches) of the det_gj launches recorded since kernel_timing(True)."""
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    check(load_library().pdb_kernel_timing_read(ctypes.byref(ms), ctypes.byref(n)), "kernel timing")
+    return ms.value, n.value
 
 
 def mulmod_peak(p: int, variant: int) -> float:

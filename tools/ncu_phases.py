@@ -78,18 +78,29 @@ def main():
             return "P"
         return "other"
     ph = collections.defaultdict(collections.Counter)
+    stall = collections.defaultdict(collections.Counter)
+    reasons = [c for c in rows[0] if c.startswith("stall_") and "Not Issued" not in c]
     for r in rows:
         _, lines = lmap.get(int(r["Address"], 16) - base, ("", []))
         m = re.match(r"\s*(@!?U?P\w+\s+)?([A-Z][A-Z0-9_.]+)", r["Source"])
         op = m.group(2) if m else "?"
         w = W.get(op, 2.0 if op.startswith("IMAD") else 1.0)
         ph[phase(lines)][op] += w * num(r["Instructions Executed"])
+        stall[phase(lines)]["ALL"] += num(r.get("Warp Stall Sampling (All Samples)", "0"))
+        for c in reasons:
+            stall[phase(lines)][c[6:]] += num(r[c])
     tot = sum(sum(c.values()) for c in ph.values())
     for k, c in sorted(ph.items(), key=lambda kv: -sum(kv[1].values())):
         s = sum(c.values())
         print("%-6s %5.1f%%  %7.0f weighted warp-inst/det   top: %s" % (
             k, 100 * s / tot, s / nd, ", ".join("%s %.0f" % (o, v / nd) for o, v in c.most_common(6))))
     print("total weighted SMSP-cycles per det (sum over SMSPs):", tot / nd)
+    sall = sum(c["ALL"] for c in stall.values()) or 1
+    print("warp-state samples per phase (share of all samples; top reasons within the phase):")
+    for k, c in sorted(stall.items(), key=lambda kv: -kv[1]["ALL"]):
+        top = [(n, v) for n, v in c.most_common() if n != "ALL"][:5]
+        print("%-6s %5.1f%%   %s" % (k, 100 * c["ALL"] / sall,
+                                     ", ".join("%s %.0f%%" % (n, 100 * v / max(c["ALL"], 1)) for n, v in top)))
 
 
 if __name__ == "__main__":
