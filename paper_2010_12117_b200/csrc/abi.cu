@@ -92,7 +92,7 @@ const Twiddles* ctx_twiddles(PrimeCtx* ctx, int N) {
   const uint64_t w = powmod64(ctx->omega, 1ull << (ctx->q - l), p);
   const uint64_t wi = powmod64(w, p - 2, p);
   const int half = N / 2 > 0 ? N / 2 : 1;
-  std::vector<uint32_t> host((size_t)4 * half + 2 * (size_t)N);
+  std::vector<uint32_t> host((size_t)4 * half + 4 * (size_t)N);
   uint32_t* f = host.data();
   uint32_t* fs = f + half;
   uint32_t* iv = fs + half;
@@ -114,6 +114,16 @@ const Twiddles* ctx_twiddles(PrimeCtx* ctx, int N) {
     fulls[j] = shoup_companion((uint32_t)c, (uint32_t)p);
     c = mulmod64(c, w, p);
   }
+  // w^-j * N^-1, j < N (the register-radix inverse folds N^-1 into its twiddles)
+  uint32_t* invn = fulls + N;
+  uint32_t* invns = invn + N;
+  const uint64_t ninv = powmod64((uint64_t)N % p, p - 2, p);
+  uint64_t d = ninv;
+  for (int j = 0; j < N; ++j) {
+    invn[j] = (uint32_t)d;
+    invns[j] = shoup_companion((uint32_t)d, (uint32_t)p);
+    d = mulmod64(d, wi, p);
+  }
   uint32_t* dev = nullptr;
   int prev = 0;
   cudaGetDevice(&prev);
@@ -131,6 +141,8 @@ const Twiddles* ctx_twiddles(PrimeCtx* ctx, int N) {
   T.inv_s = dev + 3 * half;
   T.full = dev + 4 * half;
   T.full_s = dev + 4 * half + N;
+  T.inv_full_n = dev + 4 * half + 2 * N;
+  T.inv_full_ns = dev + 4 * half + 3 * N;
   T.ninv = (uint32_t)powmod64((uint64_t)N % p, p - 2, p);
   T.ninv_s = shoup_companion(T.ninv, (uint32_t)p);
   T.N = N;

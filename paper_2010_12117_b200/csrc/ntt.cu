@@ -88,6 +88,177 @@ ntt_axis_smem(uint32_t* __restrict__ data, AxisGeom g, int N, int logN, int logT
   }
 }
 
+// ---- register-radix axis transform (N = R1 * R2 <= 256) --------------------
+// Four-step decomposition n = R2 n1 + n2, k = k1 + R1 k2:
+//   X[k1 + R1 k2] = sum_{n2} w_R2^(n2 k2) [ w_N^(n2 k1) sum_{n1} x[R2 n1 + n2] w_R1^(n1 k1) ].
+// The tile (LO lines x TI inner columns, 16-byte global loads) is staged in
+// shared memory once; pass 1 runs R2 DFT-R1s per line-column in registers and
+// writes the twiddled results back to the slots it read, pass 2 runs R1
+// DFT-R2s in registers and stores the outputs straight to global memory (N^-1
+// fused for the inverse).  Two shared-memory round trips and two barriers per
+// tile instead of log2(N) (ntt_axis_smem); twiddles are per-thread registers
+// (w_R1, w_R2 powers) plus one table load per twiddled element.  Shared layout
+// for TI = 1 (contiguous lines): one pad word per R2 words and a line stride
+// of 16 (mod 32) words, so both passes read conflict-free.
+
+#ifndef PDB_RR_MINB
+#define PDB_RR_MINB 4   // resident 256-thread CTAs per SM the register budget is sized for (4: 64 registers, measured best)
+#endif
+
+// X[k] = sum_n x[n] om^(nk), R-point radix-2 DIT in registers; tw[m] = om^m.
+template <int R>
+__device__ __forceinline__ void dft_reg(uint32_t (&x)[R], const uint32_t* tw, const uint32_t* tws, uint32_t p) {
+  constexpr int LR = R == 1 ? 0 : (R == 2 ? 1 : (R == 4 ? 2 : (R == 8 ? 3 : 4)));
+  uint32_t y[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) y[LR ? (int)(__brev((unsigned)i) >> (32 - LR)) : 0] = x[i];
+#pragma unroll
+  for (int h = 1; h < R; h <<= 1) {
+#pragma unroll
+    for (int j = 0; j < R; j += 2 * h) {
+#pragma unroll
+      for (int q = 0; q < h; ++q) {
+        const int m = q * (R / (2 * h));
+        const uint32_t u = y[j + q];
+        const uint32_t v = m ? shoup_mul(y[j + q + h], tw[m], tws[m], p) : y[j + q + h];
+        y[j + q] = add_mod(u, v, p);
+        y[j + q + h] = sub_mod(u, v, p);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) x[i] = y[i];
+}
+
+// shared-memory slot of (line lo, axis index n, column t); LS = words per line.
+// TI = 1: one pad word per R2 words (pass 2 reads R2 consecutive slots per
+// thread).  1 < TI < 32: 16 pad words per R2 rows, so the two k1 (or n2) rows
+// a warp touches in one instruction fall in opposite bank halves.
+template <int R2>
+__device__ __forceinline__ int rr_pos(int lo, int n, int t, int TI, int LS) {
+  return TI == 1 ? lo * LS + n + n / R2 : lo * LS + n * TI + t + (TI < 32 ? (n / R2) * 16 : 0);
+}
+
+template <bool INV, int R1, int R2>
+__global__ void __launch_bounds__(256, PDB_RR_MINB)
+ntt_axis_rr(uint32_t* __restrict__ data, AxisGeom g, int logTI, int logLO, int LS,
+            const uint32_t* __restrict__ full, const uint32_t* __restrict__ fulls,
+            const uint32_t* __restrict__ invn, const uint32_t* __restrict__ invns, uint32_t p) {
+  constexpr int N = R1 * R2;
+  extern __shared__ __align__(16) uint32_t sm[];
+  // twiddle table of the pass-1 factors (and the DFT constants) for this direction:
+  // tw[e] = w_N^(+-e), e < N; the inverse folds N^-1 into every pass-1 factor
+  __shared__ uint32_t tw[N], tws[N];
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    const int ee = INV ? (N - e) & (N - 1) : e;
+    uint32_t v = __ldg(full + ee), vs = __ldg(fulls + ee);
+    tw[e] = v;
+    tws[e] = vs;
+  }
+  // the inverse's N^-1 rides on the pass-1 factors: a separate scaled table
+  __shared__ uint32_t twn[INV ? N : 1], twns[INV ? N : 1];
+  if constexpr (INV) {
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+      twn[e] = __ldg(invn + e);
+      twns[e] = __ldg(invns + e);
+    }
+  }
+  const int TI = 1 << logTI, LO = 1 << logLO;
+  const int64_t tchunks = (g.inner + TI - 1) >> logTI;
+  const int64_t ntiles = ((g.active_outer + LO - 1) >> logLO) * tchunks;
+  const int cols = LO * TI;            // line-columns per tile
+  constexpr int LOGN = R1 * R2 == 1 ? 0 : __builtin_ctz(R1 * R2);
+  __shared__ int64_t line_base[64];
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t oc0 = (tile / tchunks) << logLO;
+    const int64_t t0 = (tile - (tile / tchunks) * tchunks) << logTI;
+    if (threadIdx.x < LO) {
+      const int64_t oc = oc0 + threadIdx.x;
+      line_base[threadIdx.x] = oc < g.active_outer ? outer_offset(oc, g) * (int64_t)N * g.inner + t0 : -1;
+    }
+    __syncthreads();
+    // load: 16-byte vectors along the contiguous direction (t, or n when TI = 1)
+    if (TI >= 4 && (g.inner & 3) == 0) {
+      for (int w = threadIdx.x; w < (N << (logTI + logLO)) / 4; w += blockDim.x) {
+        const int t = (w << 2) & (TI - 1);
+        const int n = ((w << 2) >> logTI) & (N - 1);
+        const int lo = (w << 2) >> (logTI + LOGN);
+        const int64_t base = line_base[lo];
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (base >= 0 && t0 + t < g.inner) v = *reinterpret_cast<const uint4*>(data + base + (int64_t)n * g.inner + t);
+        *reinterpret_cast<uint4*>(sm + rr_pos<R2>(lo, n, t, TI, LS)) = v;
+      }
+    } else if (TI == 1 && g.inner == 1 && N >= 4) {
+      for (int w = threadIdx.x; w < (N << logLO) / 4; w += blockDim.x) {
+        const int n = (w << 2) & (N - 1);
+        const int lo = (w << 2) >> LOGN;
+        const int64_t base = line_base[lo];
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (base >= 0) v = *reinterpret_cast<const uint4*>(data + base + n);
+        sm[rr_pos<R2>(lo, n, 0, 1, LS)] = v.x;
+        sm[rr_pos<R2>(lo, n + 1, 0, 1, LS)] = v.y;
+        sm[rr_pos<R2>(lo, n + 2, 0, 1, LS)] = v.z;
+        sm[rr_pos<R2>(lo, n + 3, 0, 1, LS)] = v.w;
+      }
+    } else {
+      for (int w = threadIdx.x; w < (N << (logTI + logLO)); w += blockDim.x) {
+        const int t = w & (TI - 1);
+        const int n = (w >> logTI) & (N - 1);
+        const int lo = w >> (logTI + LOGN);
+        const int64_t base = line_base[lo];
+        uint32_t v = 0;
+        if (base >= 0 && t0 + t < g.inner) v = data[base + (int64_t)n * g.inner + t];
+        sm[rr_pos<R2>(lo, n, t, TI, LS)] = v;
+      }
+    }
+    __syncthreads();
+    // pass 1: item = (line-column c, n2); DFT-R1 over n1, twiddle w_N^(n2 k1), back in place
+    for (int it = threadIdx.x; it < cols * R2; it += blockDim.x) {
+      // TI = 1: n2 fastest (consecutive slots of a line); else the column t fastest
+      const int c = TI == 1 ? it / R2 : it % cols, n2 = TI == 1 ? it % R2 : it / cols;
+      const int t = c & (TI - 1), lo = c >> logTI;
+      uint32_t x[R1];
+#pragma unroll
+      for (int n1 = 0; n1 < R1; ++n1) x[n1] = sm[rr_pos<R2>(lo, R2 * n1 + n2, t, TI, LS)];
+      {
+        uint32_t c1[R1 > 1 ? R1 / 2 : 1], c1s[R1 > 1 ? R1 / 2 : 1];
+#pragma unroll
+        for (int m = 0; m < R1 / 2; ++m) { c1[m] = tw[m * R2]; c1s[m] = tws[m * R2]; }
+        dft_reg<R1>(x, c1, c1s, p);
+      }
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) {
+        const int e = (n2 * k1) & (N - 1);
+        if constexpr (INV) x[k1] = shoup_mul(x[k1], twn[e], twns[e], p);
+        else if (k1 && n2) x[k1] = shoup_mul(x[k1], tw[e], tws[e], p);
+      }
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) sm[rr_pos<R2>(lo, R2 * k1 + n2, t, TI, LS)] = x[k1];
+    }
+    __syncthreads();
+    // pass 2: item = (line-column c, k1); DFT-R2 over n2 -> outputs k1 + R1 k2, straight to HBM
+    for (int it = threadIdx.x; it < cols * R1; it += blockDim.x) {
+      const int c = TI == 1 ? it / R1 : it % cols, k1 = TI == 1 ? it % R1 : it / cols;
+      const int t = c & (TI - 1), lo = c >> logTI;
+      uint32_t y[R2];
+#pragma unroll
+      for (int n2 = 0; n2 < R2; ++n2) y[n2] = sm[rr_pos<R2>(lo, R2 * k1 + n2, t, TI, LS)];
+      if constexpr (R2 > 1) {
+        uint32_t c2[R2 / 2], c2s[R2 / 2];
+#pragma unroll
+        for (int m = 0; m < R2 / 2; ++m) { c2[m] = tw[m * R1]; c2s[m] = tws[m * R1]; }
+        dft_reg<R2>(y, c2, c2s, p);
+      }
+      const int64_t base = line_base[lo];
+      if (base >= 0 && t0 + t < g.inner) {
+#pragma unroll
+        for (int k2 = 0; k2 < R2; ++k2) data[base + (int64_t)(k1 + R1 * k2) * g.inner + t] = y[k2];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---- global-memory fallback for very long axes (N > PDB_SMEM_NTT_MAX) -------
 __global__ void ntt_bitrev_global(uint32_t* __restrict__ data, AxisGeom g, int N, int logN) {
   const int64_t lines = g.active_outer * g.inner;
@@ -254,6 +425,41 @@ int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t
   }
   const uint32_t* tw = inverse ? T->inv : T->fwd;
   const uint32_t* tws = inverse ? T->inv_s : T->fwd_s;
+  if (N >= 2 && N <= 256 && !getenv("PDB_NTT_RADIX2")) {
+    // register-radix kernel: N = R1 * R2 (R1 = min(N, 16)); tiles of ~4096 words
+    // tiles of ~4096-8192 words: up to 32 inner columns (128-byte rows), lines to fill
+    int logTI = 0;
+    while (logTI < 5 && ((int64_t)2 << logTI) <= g.inner) ++logTI;
+    int logLO = 0;
+    while (logLO < 6 && ((int64_t)N << (logTI + logLO + 1)) <= 4096 && ((int64_t)2 << logLO) <= g.active_outer)
+      ++logLO;
+    const int R1 = N < 16 ? N : 16, R2 = N / R1;
+    int LS;       // words per line in shared memory (rr_pos)
+    if (logTI == 0) {
+      LS = N + N / R2;
+      LS += ((16 - LS % 32) + 32) % 32;   // consecutive lines in opposite bank halves
+    } else {
+      LS = (N << logTI) + (logTI < 5 ? (N / R2) * 16 : 0);
+    }
+    const int64_t tiles = ((g.active_outer + (1 << logLO) - 1) >> logLO) * ((g.inner + (1 << logTI) - 1) >> logTI);
+    const size_t smem = sizeof(uint32_t) * ((size_t)LS << logLO);
+    int grid = (int)(tiles < (int64_t)ctx->sms * 16 ? tiles : (int64_t)ctx->sms * 16);
+    const uint32_t* full = T->full;
+    const uint32_t* fulls = T->full_s;
+    const uint32_t p = (uint32_t)ctx->p;
+#define PDB_RR(A, B)                                                                                             \
+  if (R1 == A && R2 == B) {                                                                                       \
+    if (inverse)                                                                                                  \
+      ntt_axis_rr<true, A, B><<<grid, 256, smem, st>>>(data, g, logTI, logLO, LS, full, fulls, T->inv_full_n, T->inv_full_ns, p); \
+    else                                                                                                          \
+      ntt_axis_rr<false, A, B><<<grid, 256, smem, st>>>(data, g, logTI, logLO, LS, full, fulls, T->inv_full_n, T->inv_full_ns, p); \
+  }
+    PDB_RR(2, 1) PDB_RR(4, 1) PDB_RR(8, 1) PDB_RR(16, 1)
+    PDB_RR(16, 2) PDB_RR(16, 4) PDB_RR(16, 8) PDB_RR(16, 16)
+#undef PDB_RR
+    count_launch();
+    return check_launch("ntt_axis_rr");
+  }
   if (N <= PDB_SMEM_NTT_MAX) {
     int logTI = 0;   // inner columns per tile: a power of two <= min(inner, 32)
     while (logTI < 5 && (int64_t)2 << logTI <= g.inner && ((int64_t)N << (logTI + 1)) <= PDB_SMEM_NTT_MAX) ++logTI;

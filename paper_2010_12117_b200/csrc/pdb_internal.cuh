@@ -23,6 +23,8 @@ struct Twiddles {
   uint32_t* inv_s = nullptr;
   uint32_t* full = nullptr;   // w^c, c < N (node abscissae for fused evaluation)
   uint32_t* full_s = nullptr;
+  uint32_t* inv_full_n = nullptr;   // w^-c N^-1, c < N (register-radix inverse twiddles)
+  uint32_t* inv_full_ns = nullptr;
   uint32_t ninv = 1, ninv_s = 0;  // N^-1 and its companion
 };
 
