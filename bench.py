@@ -319,6 +319,14 @@ def poly_e2e(world, rank, cpu=True):
                                       "crt": timings.crt},
                "nonzero_terms": sum(1 for c in result.coeffs if c),
                "reference_dev_container_s": REFERENCE_DEV_SECONDS.get(name)}
+        if name in ("C3", "C5") and rank == 0:
+            # the result printer (reference parsing.py:211-225 via cli.py:61-83), native
+            from paper_2010_12117_b200 import format_polynomial
+            t0 = time.perf_counter()
+            text = format_polynomial(result, result.axis_vars)
+            rec["format_s"] = time.perf_counter() - t0
+            rec["format_chars"] = len(text)
+            del text
         del result
         if cpu and rank == 0 and world == 1:
             c = cpu_poly(name, m, pl, threads)

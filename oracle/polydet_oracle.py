@@ -20,6 +20,7 @@ Each function names the reference code it restates:
 * `crt_combine`        crt.py:94-130        (mixed radix digits + Horner + signed lift)
 * `reduce_entry`       tensor.py:214-237    (reduce_mod + pad_to of one entry)
 * `run_pipeline`       pipeline.py:323-404  (per prime FFT -> DET -> IFFT, then CRT)
+* `format_polynomial`  parsing.py:197-225   (canonical result text; tensor.py:25-32 normalisation)
 
 All arithmetic is int64 with p <= 3037000499 (p^2 < 2^63), as on the
 reference's fast path (`modular.py:15-19`, `tensor.py:152-154`).
@@ -224,3 +225,33 @@ def run_pipeline(unique_terms, entry_ids, r, shape, primes, workers=1):
         values = det_grid(grids, r, p, entry_ids, workers=workers)
         residues.append(ntt_multi(values, shape, p, omega, q, inverse=True))
     return crt_combine(residues, [p for p, _, _ in primes]), residues
+
+
+def format_polynomial(terms, variables):
+    """parsing.py:197-225: graded lexicographic order (total degree, then the
+    exponent tuple), highest first; tensor.py:25-32 combines like monomials
+    and drops zeros first."""
+    pairs = terms.items() if hasattr(terms, "items") else terms
+    acc = {}
+    for exps, coeff in pairs:
+        e = tuple(int(x) for x in exps)
+        acc[e] = acc.get(e, 0) + int(coeff)
+    norm = {e: c for e, c in acc.items() if c}
+    if not norm:
+        return "0"
+    variables = tuple(variables)
+    out = []
+    for i, (exps, coeff) in enumerate(sorted(norm.items(), key=lambda it: (sum(it[0]), it[0]), reverse=True)):
+        parts = []
+        for var, e in zip(variables, exps):
+            if e == 1:
+                parts.append(var)
+            elif e > 1:
+                parts.append("%s^%d" % (var, e))
+        mag = abs(coeff)
+        text = str(mag) if not parts else ("*".join(parts) if mag == 1 else "%d*%s" % (mag, "*".join(parts)))
+        if i == 0:
+            out.append("-" + text if coeff < 0 else text)
+        else:
+            out.append(("- " if coeff < 0 else "+ ") + text)
+    return " ".join(out)

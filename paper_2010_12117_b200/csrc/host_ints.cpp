@@ -147,6 +147,275 @@ done:
   return out;
 }
 
+// ---- format_terms: the reference's canonical polynomial text at 10^5-10^7 terms ----
+//
+// format_terms(terms: dict[tuple[int, ...], int], variables: tuple[str, ...], threads: int) -> str
+// byte-identical to parsing.py:197-225 (format_polynomial): terms sorted by
+// (total degree, exponent tuple) descending; a term prints its variables with
+// exponent 1 as `x`, > 1 as `x^e` (others omitted), joined by `*`, prefixed by
+// `|c|*` unless |c| = 1 (a constant prints |c|); the first term carries `-` for
+// a negative coefficient, later ones are joined as ` + t` / ` - t`; no terms
+// prints `0`.  Keys must be tuples of exact ints of one arity and values exact
+// ints (the caller normalises anything else first, tensor.py:25-32); zero
+// coefficients are skipped.  The sort and the text run in C++ (the decimal
+// digits of big coefficients in `threads` threads on CPython 3.12/3.13).
+#include <algorithm>
+#include <deque>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+struct FmtTerm {
+  const int64_t* e;   // exponents (arity k)
+  int64_t deg;
+  PyObject* c;        // borrowed coefficient
+  bool neg, one;      // c < 0, |c| == 1 (read with the GIL, before the threads start)
+  const std::string* dec;   // |c| in decimal when made with the GIL (huge or portable), else null
+};
+
+// |v| in decimal, appended to out.  Direct path: 30-bit digits -> base 10^9 by
+// schoolbook division (no Python API: safe in worker threads).
+static bool append_abs_decimal(std::string& out, PyObject* v) {
+#ifdef PDB_DIRECT_LONG
+  const PyLongObject* op = reinterpret_cast<const PyLongObject*>(v);
+  const uintptr_t tag = op->long_value.lv_tag;
+  Py_ssize_t nd = (Py_ssize_t)(tag >> _PyLong_NON_SIZE_BITS);
+  const digit* d = op->long_value.ob_digit;
+  if (nd == 0) { out.push_back('0'); return true; }
+  if (nd <= 2) {
+    unsigned long long m = d[0] | (nd == 2 ? (unsigned long long)d[1] << PyLong_SHIFT : 0ull);
+    char buf[24];
+    int n = 0;
+    do { buf[n++] = (char)('0' + m % 10); m /= 10; } while (m);
+    while (n) out.push_back(buf[--n]);
+    return true;
+  }
+  if (nd > 80) return false;
+  uint32_t w[80];                        // little-endian base 2^30
+  for (Py_ssize_t i = 0; i < nd; ++i) w[i] = d[i];
+  uint32_t chunks[100];                  // base 10^9, little-endian
+  int nc = 0;
+  Py_ssize_t top = nd;
+  while (top > 0) {
+    uint64_t rem = 0;
+    for (Py_ssize_t i = top - 1; i >= 0; --i) {
+      const uint64_t cur = (rem << PyLong_SHIFT) | w[i];
+      const uint64_t q = cur / 1000000000ull;
+      w[i] = (uint32_t)q;
+      rem = cur - q * 1000000000ull;
+    }
+    chunks[nc++] = (uint32_t)rem;
+    while (top > 0 && w[top - 1] == 0) --top;
+  }
+  char buf[16];
+  int n = 0;
+  uint32_t x = chunks[nc - 1];
+  do { buf[n++] = (char)('0' + x % 10); x /= 10; } while (x);
+  while (n) out.push_back(buf[--n]);
+  for (int i = nc - 2; i >= 0; --i) {
+    x = chunks[i];
+    char nine[9];
+    for (int j = 8; j >= 0; --j) { nine[j] = (char)('0' + x % 10); x /= 10; }
+    out.append(nine, 9);
+  }
+  return true;
+#else
+  (void)out; (void)v;
+  return false;
+#endif
+}
+
+struct FmtCtx {
+  std::vector<FmtTerm>* terms;
+  int k;
+  const std::vector<std::string>* names;
+};
+
+static void format_range(const FmtCtx& cx, size_t lo, size_t hi, std::string& out) {
+  const std::vector<FmtTerm>& T = *cx.terms;
+  for (size_t i = lo; i < hi; ++i) {
+    const FmtTerm& t = T[i];
+    const bool neg = t.neg;
+    if (i == 0) {
+      if (neg) out.push_back('-');
+    } else {
+      out.append(neg ? " - " : " + ");
+    }
+    bool body = false;
+    for (int a = 0; a < cx.k; ++a) if (t.e[a] >= 1) { body = true; break; }
+    const bool one = body && t.one;
+    if (!one) {
+      if (t.dec) out.append(*t.dec);
+      else append_abs_decimal(out, t.c);
+      if (body) out.push_back('*');
+    }
+    bool first = true;
+    for (int a = 0; a < cx.k; ++a) {
+      const int64_t e = t.e[a];
+      if (e < 1) continue;
+      if (!first) out.push_back('*');
+      first = false;
+      out.append((*cx.names)[a]);
+      if (e > 1) {
+        out.push_back('^');
+        out.append(std::to_string((long long)e));
+      }
+    }
+  }
+}
+
+}  // namespace
+
+static PyObject* format_terms(PyObject*, PyObject* args) {
+  PyObject *terms, *variables;
+  int threads = 1;
+  if (!PyArg_ParseTuple(args, "O!O!i", &PyDict_Type, &terms, &PyTuple_Type, &variables, &threads)) return nullptr;
+  const int k = (int)PyTuple_GET_SIZE(variables);
+  std::vector<std::string> names((size_t)k);
+  for (int a = 0; a < k; ++a) {
+    Py_ssize_t n = 0;
+    const char* u = PyUnicode_AsUTF8AndSize(PyTuple_GET_ITEM(variables, a), &n);
+    if (!u) return nullptr;
+    names[(size_t)a].assign(u, (size_t)n);
+  }
+  const Py_ssize_t count = PyDict_GET_SIZE(terms);
+  std::vector<int64_t> exps;
+  exps.reserve((size_t)count * (size_t)(k > 0 ? k : 1));
+  std::vector<FmtTerm> T;
+  T.reserve((size_t)count);
+  Py_ssize_t pos = 0;
+  PyObject *key, *val;
+  // first pass: exponents (the vector must not reallocate once pointers are taken)
+  std::deque<std::string> decs;   // stable addresses
+  PyObject* zero_obj = PyLong_FromLong(0);
+  PyObject* one_obj = PyLong_FromLong(1);
+  PyObject* mone_obj = PyLong_FromLong(-1);
+  struct Drop { PyObject *a, *b, *c; ~Drop() { Py_XDECREF(a); Py_XDECREF(b); Py_XDECREF(c); } } drop{zero_obj, one_obj, mone_obj};
+  while (PyDict_Next(terms, &pos, &key, &val)) {
+    if (!PyTuple_CheckExact(key) || PyTuple_GET_SIZE(key) != k || !PyLong_CheckExact(val)) {
+      PyErr_SetString(PyExc_TypeError, "format_terms: keys must be k-tuples of ints and values ints");
+      return nullptr;
+    }
+    for (int a = 0; a < k; ++a) {
+      PyObject* x = PyTuple_GET_ITEM(key, a);
+      if (!PyLong_CheckExact(x)) {
+        PyErr_SetString(PyExc_TypeError, "format_terms: exponents must be ints");
+        return nullptr;
+      }
+      const long long e = PyLong_AsLongLong(x);
+      if (e == -1 && PyErr_Occurred()) return nullptr;
+      exps.push_back((int64_t)e);
+    }
+    if (k == 0) exps.push_back(0);
+    const int zero = PyObject_Not(val);
+    if (zero < 0) return nullptr;
+    if (zero) { exps.resize(exps.size() - (size_t)(k > 0 ? k : 1)); continue; }
+#ifdef PDB_DIRECT_LONG
+    const uintptr_t tag = reinterpret_cast<const PyLongObject*>(val)->long_value.lv_tag;
+    const int neg = (tag & 3) == 2;
+    const int one = (tag >> _PyLong_NON_SIZE_BITS) == 1 && reinterpret_cast<const PyLongObject*>(val)->long_value.ob_digit[0] == 1;
+#else
+    const int neg = PyObject_RichCompareBool(val, zero_obj, Py_LT);
+    const int one = PyObject_RichCompareBool(val, one_obj, Py_EQ) == 1 ||
+                    PyObject_RichCompareBool(val, mone_obj, Py_EQ) == 1;
+    if (neg < 0) return nullptr;
+#endif
+    const std::string* dec = nullptr;
+#ifdef PDB_DIRECT_LONG
+    const bool huge = (reinterpret_cast<const PyLongObject*>(val)->long_value.lv_tag >> _PyLong_NON_SIZE_BITS) > 80;
+#else
+    const bool huge = true;   // portable build: every magnitude through the public API
+#endif
+    if (huge) {
+      PyObject* a = PyNumber_Absolute(val);
+      PyObject* str = a ? PyObject_Str(a) : nullptr;
+      Py_XDECREF(a);
+      if (!str) return nullptr;
+      Py_ssize_t sn = 0;
+      const char* u = PyUnicode_AsUTF8AndSize(str, &sn);
+      decs.emplace_back(u, (size_t)sn);
+      Py_DECREF(str);
+      dec = &decs.back();
+    }
+    T.push_back(FmtTerm{nullptr, 0, val, neg == 1, one != 0, dec});
+  }
+  const size_t stride = (size_t)(k > 0 ? k : 1);
+  for (size_t i = 0; i < T.size(); ++i) {
+    T[i].e = exps.data() + i * stride;
+    int64_t d = 0;
+    for (int a = 0; a < k; ++a) d += T[i].e[a];
+    T[i].deg = d;
+  }
+  if (T.empty()) return PyUnicode_FromString("0");
+  // graded lexicographic, highest first: key (deg, e_0, ..., e_{k-1}) descending
+  auto later = [k](const FmtTerm& x, const FmtTerm& y) {
+    if (x.deg != y.deg) return x.deg > y.deg;
+    for (int a = 0; a < k; ++a)
+      if (x.e[a] != y.e[a]) return x.e[a] > y.e[a];
+    return false;
+  };
+  const int nthreads = std::max(1, std::min(threads, 64));
+  Py_BEGIN_ALLOW_THREADS
+  {
+    // chunks sorted in parallel, then merged pairwise (each round in parallel)
+    const size_t n = T.size();
+    const int ns = n < 100000 ? 1 : nthreads;
+    std::vector<size_t> cut((size_t)ns + 1);
+    for (int j = 0; j <= ns; ++j) cut[(size_t)j] = n * (size_t)j / (size_t)ns;
+    std::vector<std::thread> pool;
+    for (int j = 0; j < ns; ++j)
+      pool.emplace_back([&, j]() { std::sort(T.begin() + cut[(size_t)j], T.begin() + cut[(size_t)j + 1], later); });
+    for (auto& th : pool) th.join();
+    for (size_t width = 1; width < (size_t)ns; width *= 2) {
+      std::vector<std::thread> mp;
+      for (size_t j = 0; j + width < (size_t)ns; j += 2 * width) {
+        const size_t lo = cut[j], mid = cut[j + width], hi = cut[std::min(j + 2 * width, (size_t)ns)];
+        mp.emplace_back([&, lo, mid, hi]() { std::inplace_merge(T.begin() + lo, T.begin() + mid, T.begin() + hi, later); });
+      }
+      for (auto& th : mp) th.join();
+    }
+  }
+  Py_END_ALLOW_THREADS
+  const int nt = T.size() < 20000 ? 1 : nthreads;
+
+  FmtCtx cx{&T, k, &names};
+  std::vector<std::string> parts((size_t)nt);
+  // the coefficient objects are immutable and kept alive by the dict for the
+  // whole call: worker threads read their digits without the GIL
+  Py_BEGIN_ALLOW_THREADS
+  std::vector<std::thread> pool;
+  for (int j = 0; j < nt; ++j) {
+    const size_t lo = T.size() * (size_t)j / (size_t)nt, hi = T.size() * (size_t)(j + 1) / (size_t)nt;
+    auto job = [&cx, &parts, j, lo, hi]() { format_range(cx, lo, hi, parts[(size_t)j]); };
+    if (j + 1 < nt) pool.emplace_back(job);
+    else job();
+  }
+  for (auto& th : pool) th.join();
+  Py_END_ALLOW_THREADS
+  size_t total = 0;
+  for (auto& s : parts) total += s.size();
+  bool ascii = true;
+  for (auto& nm : names)
+    for (unsigned char ch : nm) ascii = ascii && ch < 128;
+  if (ascii) {   // digits, signs and ASCII names: one copy into the str object
+    PyObject* out = PyUnicode_New((Py_ssize_t)total, 127);
+    if (!out) return nullptr;
+    char* dst = reinterpret_cast<char*>(PyUnicode_1BYTE_DATA(out));
+    for (auto& s : parts) {
+      std::memcpy(dst, s.data(), s.size());
+      dst += s.size();
+      std::string().swap(s);
+    }
+    return out;
+  }
+  std::string all;
+  all.reserve(total);
+  for (auto& s : parts) { all.append(s); std::string().swap(s); }
+  return PyUnicode_DecodeUTF8(all.data(), (Py_ssize_t)all.size(), "strict");
+}
+
 static PyObject* ints_from_limbs(PyObject*, PyObject* args) { return build(args, false); }
 static PyObject* ints_from_limbs_portable(PyObject*, PyObject* args) { return build(args, true); }
 
@@ -164,6 +433,8 @@ static PyMethodDef methods[] = {
     {"ints_from_limbs_portable", ints_from_limbs_portable, METH_VARARGS,
      "the same through the public C API only (int.from_bytes): the path on other CPython ABIs"},
     {"direct_path", direct_path, METH_NOARGS, "True if this build writes PyLong digits directly"},
+    {"format_terms", format_terms, METH_VARARGS,
+     "format_terms(terms, variables, threads) -> the reference's canonical polynomial text (parsing.py:211-225)"},
     {nullptr, nullptr, 0, nullptr}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_pdb_host", "native result materialisation", -1, methods};

@@ -459,7 +459,38 @@ def c4_full(names=None):
         _write("c4_results.json", have)
 
 
+def format_cases():
+    """The reference's canonical text (parsing.py:211-225) of every pinned run
+    result, of the reference test forms, and of random term sets with big,
+    negative, unit and zero coefficients and negative/zero exponents."""
+    from polydet.parsing import format_polynomial as ref_format
+
+    runs = json.loads((HERE / "runs.json").read_text())
+    cases = []
+    for run in runs:
+        names = tuple(run["input"]["variables"])
+        terms = {tuple(e): int(c) for e, c in run["terms"]}
+        cases.append({"name": run["name"], "variables": list(names), "terms": _terms_json(terms),
+                      "text": ref_format(terms, names)})
+    rng = random.Random(211)
+    for n in range(40):
+        k = rng.randint(0, 4)
+        names = tuple("abcdxyz"[:k])
+        terms = {}
+        for _ in range(rng.randint(0, 60)):
+            e = tuple(rng.choice([0, 0, 1, 1, 2, 3, 7, 12, -1]) for _ in range(k))
+            c = rng.choice([0, 1, -1, rng.randint(-10**6, 10**6), rng.randint(-2**600, 2**600),
+                            rng.randint(-2**64, 2**64)])
+            terms[e] = c
+        cases.append({"name": "random_%d" % n, "variables": list(names), "terms": _terms_json(terms),
+                      "text": ref_format(terms, names)})
+    _write("format.json", cases)
+
+
 if __name__ == "__main__":
+    if "--format" in sys.argv:
+        format_cases()
+        sys.exit(0)
     if "--acceptance" in sys.argv:
         acceptance_exact()
         sys.exit(0)

@@ -39,3 +39,33 @@ def test_rejects_inconsistent_buffers():
         host.ints_from_limbs(limbs, np.arange(2, dtype=np.int64), np.zeros(2, dtype=np.uint8), 5, 2)
     with pytest.raises(IndexError):
         host.ints_from_limbs(limbs, np.array([0, 1, 9], dtype=np.int64), np.zeros(3, dtype=np.uint8), 5, 2)
+
+
+def test_formatter_portable_build_agrees(tmp_path):
+    """format_terms built without the direct-PyLong code (the path on other
+    CPython ABIs) prints the same text as the direct build and the oracle,
+    including coefficients beyond the direct path's 2400-bit fast case."""
+    import importlib.util
+    import shutil
+    import subprocess
+    import sysconfig
+
+    from helpers import ROOT
+    from oracle import polydet_oracle as O
+
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    out = tmp_path / ("_pdb_host" + sysconfig.get_config_var("EXT_SUFFIX"))
+    subprocess.run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-DPDB_NO_DIRECT_LONG",
+                    "-I" + sysconfig.get_paths()["include"], "-o", str(out),
+                    str(ROOT / "paper_2010_12117_b200" / "csrc" / "host_ints.cpp")], check=True)
+    spec = importlib.util.spec_from_file_location("_pdb_host", out)
+    portable = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(portable)
+    assert portable.direct_path() is False
+    rng = random.Random(3)
+    terms = {(rng.randint(0, 5), rng.randint(0, 5)): rng.choice([1, -1, 0, rng.randint(-2**3000, 2**3000),
+                                                                 rng.randint(-99, 99)]) for _ in range(3000)}
+    want = O.format_polynomial(terms, ("x", "y"))
+    assert portable.format_terms(terms, ("x", "y"), 4) == want
+    assert native.host_module().format_terms(terms, ("x", "y"), 4) == want
