@@ -152,6 +152,14 @@ int32_t pdb_crt_mrc_sel_u32(const uint32_t* residues, int32_t nprimes, int64_t s
                             const uint32_t* primes, const int64_t* index, int64_t count, uint32_t* limbs,
                             int32_t L, uint8_t* neg, int32_t* width, void* stream);
 
+/* Result materialisation (reference crt.py:122-130 builds Python ints): the
+ * |X| limb rows [count][width] (row stride `stride` u32) re-cut into CPython's
+ * 30-bit digits [count][ndigits] (ndigits >= ceil(32 width / 30), <= 255) plus
+ * the significant digit count per row, on the device; the host then makes each
+ * int with one allocation and one copy.  No host synchronisation. */
+int32_t pdb_limbs_to_digits30(const uint32_t* limbs, int64_t count, int32_t width, int64_t stride,
+                              uint32_t* digits, int32_t ndigits, uint8_t* digit_count, void* stream);
+
 /* Integer-pipe peak of an update primitive (no memory traffic), in updates/s.
  * variant 0 = Shoup mul-mod + sub-mod, 1 = delayed 64-bit MAC (9 MACs + one REDC,
  * the det kernel's trailing update: updates = MACs), 2 = raw accumulating

@@ -132,8 +132,7 @@ def device_lift(residues_dev, primes, n: int, stride: int) -> list:
         width = max(int(wbuf.item()), 1)
         idx_h = np.ascontiguousarray(idx[:count].cpu().numpy())
         neg_h = np.ascontiguousarray(neg[:count].cpu().numpy())
-        with _PIN_LOCK:   # the staging buffer is shared; the ints are built before it is reused
-            return host.ints_from_limbs(_to_host(limbs[:count, :width]), idx_h, neg_h, int(n), int(width))
+        return _build_ints(host, limbs, count, width, L, idx_h, neg_h, n)
     limbs = torch.empty((n, L), dtype=torch.int32, device=dev)
     neg = torch.empty(n, dtype=torch.uint8, device=dev)
     scratch = native.scratch_tensor(native.crt_scratch_bytes(P, wide), dev)
@@ -178,8 +177,26 @@ def sharded_lift(block, primes, n: int, lo: int, rank: int, size: int) -> tuple:
     g_limbs, g_idx, g_neg = shard.gather_compact(count, limbs, idx, neg, width, rank, size)
     idx_h = np.ascontiguousarray(g_idx.cpu().numpy())
     neg_h = np.ascontiguousarray(g_neg.cpu().numpy())
+    g_limbs = g_limbs.contiguous()
+    return _build_ints(native.host_module(), g_limbs, g_limbs.shape[0], width, g_limbs.shape[1], idx_h, neg_h, n)
+
+
+def _build_ints(host, limbs, count: int, width: int, stride: int, idx_h, neg_h, n: int) -> tuple:
+    """Compact |X| limb rows on the device -> the tuple of n Python ints.  On
+    CPython 3.12/3.13 the device re-cuts the rows into CPython's 30-bit digits
+    (pdb_limbs_to_digits30) so the host only allocates and copies; elsewhere
+    the limb rows go through the portable constructor."""
+    torch = native._torch()
+    if count and host.direct_path() and (count < 2 or bool(np.all(idx_h[1:] > idx_h[:-1]))):
+        D = (32 * width + 29) // 30
+        digits = torch.empty((count, D), dtype=torch.int32, device=limbs.device)
+        nd = torch.empty(count, dtype=torch.uint8, device=limbs.device)
+        native.limbs_to_digits30(limbs, count, width, stride, digits, D, nd)
+        nd_h = np.ascontiguousarray(nd.cpu().numpy())
+        with _PIN_LOCK:   # the staging buffer is shared; the ints are built before it is reused
+            return host.ints_from_digits(_to_host(digits), nd_h, idx_h, neg_h, int(n), int(D))
     with _PIN_LOCK:
-        return native.host_module().ints_from_limbs(_to_host(g_limbs), idx_h, neg_h, int(n), int(width))
+        return host.ints_from_limbs(_to_host(limbs[:count, :width]), idx_h, neg_h, int(n), int(width))
 
 
 _PINNED = {}

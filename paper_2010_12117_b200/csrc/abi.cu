@@ -161,6 +161,8 @@ size_t crt_scratch_bytes(int P);
 size_t crt_nonzero_scratch_bytes(int64_t n);
 int crt_nonzero(const uint32_t* res, int P, int64_t n, int64_t stride, int64_t* index, int64_t* count,
                 void* scratch, size_t scratch_bytes, cudaStream_t st);
+int limbs_to_digits(const uint32_t* limbs, int64_t count, int width, int64_t ls, uint32_t* digits, int D,
+                    uint8_t* ndig, int sms, cudaStream_t st);
 int crt_mrc_sel(const uint32_t* res, int P, const int64_t* index, int64_t count, int64_t res_stride,
                 const uint32_t* primes_host, uint32_t* limbs, int L, uint8_t* neg, int32_t* width, int sms,
                 cudaStream_t st);
@@ -511,6 +513,15 @@ int32_t pdb_crt_mrc_sel_u32(const uint32_t* residues, int32_t nprimes, int64_t s
   int sms = pdb_device_sm_count(dev);
   return crt_mrc_sel(residues, nprimes, index, count, stride, primes, limbs, L, neg, width, sms > 0 ? sms : 148,
                      (cudaStream_t)stream);
+}
+
+int32_t pdb_limbs_to_digits30(const uint32_t* limbs, int64_t count, int32_t width, int64_t stride,
+                              uint32_t* digits, int32_t ndigits, uint8_t* digit_count, void* stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = pdb_device_sm_count(dev);
+  return limbs_to_digits(limbs, count, width, stride, digits, ndigits, digit_count, sms > 0 ? sms : 148,
+                         (cudaStream_t)stream);
 }
 
 int32_t pdb_kernel_timing(int32_t enable) {

@@ -409,6 +409,52 @@ int crt_mrc(const uint32_t* res, int P, int64_t n, int64_t res_stride, const uin
   return crt_mrc_sel(res, P, nullptr, n, res_stride, primes_host, limbs, L, neg, nullptr, sms, st);
 }
 
+// |X| as u32 limb rows [count][width] (stride ls words) -> CPython's 30-bit
+// digits [count][D] (D = ceil(32 width / 30)) and the significant digit count,
+// so the host builds each int with one allocation and one copy.
+__global__ void __launch_bounds__(256)
+limbs_to_digits30(const uint32_t* __restrict__ limbs, int64_t count, int width, int64_t ls,
+                  uint32_t* __restrict__ digits, int D, uint8_t* __restrict__ ndig) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < count; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t* row = limbs + j * ls;
+    uint32_t* out = digits + j * (int64_t)D;
+    int nd = 0, used = 0, bits = 0;
+    uint64_t acc = 0;
+    for (int w = 0; w < width; ++w) {
+      acc |= (uint64_t)__ldg(row + w) << bits;
+      bits += 32;
+      while (bits >= 30) {
+        const uint32_t d = (uint32_t)acc & 0x3fffffffu;
+        out[nd++] = d;
+        if (d) used = nd;
+        acc >>= 30;
+        bits -= 30;
+      }
+    }
+    if (bits > 0) {
+      const uint32_t d = (uint32_t)acc;
+      out[nd++] = d;
+      if (d) used = nd;
+    }
+    for (; nd < D; ++nd) out[nd] = 0u;
+    ndig[j] = (uint8_t)used;
+  }
+}
+
+int limbs_to_digits(const uint32_t* limbs, int64_t count, int width, int64_t ls, uint32_t* digits, int D,
+                    uint8_t* ndig, int sms, cudaStream_t st) {
+  if (width < 1 || D < (32 * width + 29) / 30 || D > 255 || ls < width) {
+    set_error("limbs_to_digits: width %d, digit rows %d, stride %lld", width, D, (long long)ls);
+    return -2;
+  }
+  if (count <= 0) return 0;
+  const int64_t blocks = (count + 255) / 256;
+  const int grid = (int)(blocks < (int64_t)sms * 8 ? blocks : (int64_t)sms * 8);
+  limbs_to_digits30<<<grid, 256, 0, st>>>(limbs, count, width, ls, digits, D, ndig);
+  count_launch();
+  return check_launch("limbs_to_digits");
+}
+
 size_t crt_nonzero_scratch_bytes(int64_t n) {
   const int64_t nb = (n + NZ_TILE - 1) / NZ_TILE;
   return 256 + sizeof(int64_t) * (size_t)nb + (size_t)n;

@@ -416,6 +416,76 @@ static PyObject* format_terms(PyObject*, PyObject* args) {
   return PyUnicode_DecodeUTF8(all.data(), (Py_ssize_t)all.size(), "strict");
 }
 
+// ints_from_digits(digits: [count][D] u32 30-bit digits, ndig: uint8[count], index: int64[count] (ascending),
+//                  neg: uint8[count], n, D) -> tuple of n ints (the device already re-cut the limbs,
+//                  pdb_limbs_to_digits30: one allocation + one copy per int; CPython 3.12/3.13 only)
+static PyObject* ints_from_digits(PyObject*, PyObject* args) {
+#ifdef PDB_DIRECT_LONG
+  Py_buffer digits, ndig, index, neg;
+  Py_ssize_t n, D;
+  if (!PyArg_ParseTuple(args, "y*y*y*y*nn", &digits, &ndig, &index, &neg, &n, &D)) return nullptr;
+  PyObject* out = nullptr;
+  PyObject* zero = nullptr;
+  const Py_ssize_t count = index.len / (Py_ssize_t)sizeof(int64_t);
+  const uint32_t* dg = static_cast<const uint32_t*>(digits.buf);
+  const uint8_t* nd = static_cast<const uint8_t*>(ndig.buf);
+  const int64_t* ix = static_cast<const int64_t*>(index.buf);
+  const uint8_t* ng = static_cast<const uint8_t*>(neg.buf);
+  if (D < 1 || n < 0 || digits.len != count * D * 4 || ndig.len != count || neg.len != count) {
+    PyErr_SetString(PyExc_ValueError, "ints_from_digits: inconsistent buffer sizes");
+    goto done;
+  }
+  for (Py_ssize_t j = 0; j < count; ++j) {
+    if (ix[j] < 0 || ix[j] >= n || (j && ix[j] <= ix[j - 1]) || nd[j] > D) {
+      PyErr_SetString(PyExc_IndexError, "ints_from_digits: index out of range or not ascending");
+      goto done;
+    }
+  }
+  out = PyTuple_New(n);
+  if (!out) goto done;
+  zero = PyLong_FromLong(0);
+  {
+    Py_ssize_t j = 0;
+    for (Py_ssize_t i = 0; i < n; ++i) {
+      PyObject* v;
+      if (j < count && ix[j] == i) {
+        const Py_ssize_t k = nd[j];
+        const uint32_t* row = dg + (size_t)j * (size_t)D;
+        const bool negative = ng[j] != 0;
+        if (k <= 2) {
+          const long long x = k == 0 ? 0 : (long long)row[0] | (k == 2 ? (long long)row[1] << PyLong_SHIFT : 0);
+          v = PyLong_FromLongLong(negative ? -x : x);
+        } else {
+          PyLongObject* op = _PyLong_New(k);
+          if (op) {
+            std::memcpy(op->long_value.ob_digit, row, (size_t)k * sizeof(digit));
+            if (negative) op->long_value.lv_tag = ((uintptr_t)k << _PyLong_NON_SIZE_BITS) | 2;
+          }
+          v = (PyObject*)op;
+        }
+        ++j;
+        if (!v) { Py_CLEAR(out); goto done; }
+      } else {
+        Py_INCREF(zero);
+        v = zero;
+      }
+      PyTuple_SET_ITEM(out, i, v);
+    }
+  }
+done:
+  Py_XDECREF(zero);
+  PyBuffer_Release(&digits);
+  PyBuffer_Release(&ndig);
+  PyBuffer_Release(&index);
+  PyBuffer_Release(&neg);
+  return out;
+#else
+  (void)args;
+  PyErr_SetString(PyExc_NotImplementedError, "ints_from_digits needs the direct PyLong layout (CPython 3.12/3.13)");
+  return nullptr;
+#endif
+}
+
 static PyObject* ints_from_limbs(PyObject*, PyObject* args) { return build(args, false); }
 static PyObject* ints_from_limbs_portable(PyObject*, PyObject* args) { return build(args, true); }
 
@@ -433,6 +503,8 @@ static PyMethodDef methods[] = {
     {"ints_from_limbs_portable", ints_from_limbs_portable, METH_VARARGS,
      "the same through the public C API only (int.from_bytes): the path on other CPython ABIs"},
     {"direct_path", direct_path, METH_NOARGS, "True if this build writes PyLong digits directly"},
+    {"ints_from_digits", ints_from_digits, METH_VARARGS,
+     "ints_from_digits(digits, ndig, index, neg, n, D) -> tuple of n ints from device-made 30-bit digit rows"},
     {"format_terms", format_terms, METH_VARARGS,
      "format_terms(terms, variables, threads) -> the reference's canonical polynomial text (parsing.py:211-225)"},
     {nullptr, nullptr, 0, nullptr}};

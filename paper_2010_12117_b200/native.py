@@ -76,6 +76,7 @@ _SIGNATURES = {
                                      _c_vp]),
     "pdb_mulmod_peak": (_c_i32, [_c_u32, _c_i32, ctypes.POINTER(ctypes.c_double), _c_vp]),
     "pdb_kernel_timing": (_c_i32, [_c_i32]),
+    "pdb_limbs_to_digits30": (_c_i32, [_c_vp, _c_i64, _c_i32, _c_i64, _c_vp, _c_i32, _c_vp, _c_vp]),
     "pdb_kernel_timing_read": (_c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_c_i64)]),
     # the wide path (2^31 <= p < 2^62): u64 twins
     "pdb_prime_ctx_create_wide": (_c_i32, [_c_u64, _c_u64, _c_i32, ctypes.POINTER(_c_vp)]),
@@ -362,6 +363,14 @@ def crt_mrc_sel(residues, nprimes: int, stride: int, primes, index, count: int, 
 def launch_count() -> int:
     """Kernels this process has launched through the library (all devices)."""
     return int(load_library().pdb_launch_count())
+
+
+def limbs_to_digits30(limbs, count: int, width: int, stride: int, digits, ndigits: int, digit_count,
+                      stream=None):
+    """Limb rows [count][width] (row stride `stride`) -> 30-bit digit rows [count][ndigits] + counts."""
+    check(load_library().pdb_limbs_to_digits30(ptr(limbs), int(count), int(width), int(stride), ptr(digits),
+                                               int(ndigits), ptr(digit_count), stream_handle(stream)),
+          "limbs to digits")
 
 
 def kernel_timing(enable: bool) -> None:

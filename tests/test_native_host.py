@@ -69,3 +69,26 @@ def test_formatter_portable_build_agrees(tmp_path):
     want = O.format_polynomial(terms, ("x", "y"))
     assert portable.format_terms(terms, ("x", "y"), 4) == want
     assert native.host_module().format_terms(terms, ("x", "y"), 4) == want
+
+
+def test_ints_from_digits_matches_limb_path():
+    """The digit-row constructor (rows re-cut on the device by
+    pdb_limbs_to_digits30; here cut in Python) builds the same ints as the
+    limb-row one."""
+    host = native.host_module()
+    if not host.direct_path():
+        pytest.skip("direct PyLong layout only")
+    rng = random.Random(30)
+    n, width = 5000, 17
+    idx = sorted(rng.sample(range(n), 1200))
+    vals = [rng.getrandbits(rng.choice([1, 30, 31, 60, 61, 62, 200, 32 * width])) for _ in idx]
+    neg = np.array([rng.random() < 0.5 for _ in idx], dtype=np.uint8)
+    D = (32 * width + 29) // 30
+    digits = np.array([[(v >> (30 * k)) & ((1 << 30) - 1) for k in range(D)] for v in vals], dtype=np.uint32)
+    nd = np.array([(v.bit_length() + 29) // 30 for v in vals], dtype=np.uint8)
+    ix = np.array(idx, dtype=np.int64)
+    limbs = np.frombuffer(b"".join(v.to_bytes(4 * width, "little") for v in vals), dtype="<u4").reshape(-1, width)
+    want = host.ints_from_limbs(limbs, ix, neg, n, width)
+    assert host.ints_from_digits(digits, nd, ix, neg, n, D) == want
+    with pytest.raises(IndexError):
+        host.ints_from_digits(digits, nd, ix[::-1].copy(), neg, n, D)
