@@ -9,8 +9,9 @@ single-GPU configuration): 40x40 matrix, 3 variables, entry degree <= 4,
 for one prime: forward evaluation of all 1600 unique entries (partial NTT +
 fused last-axis evaluation), the 40x40 determinants mod p at the kept nodes
 (the degree bound 160 per variable needs 168 x 168 x 176 = 4.97 M of the 16.7 M
-nodes, csrc/expand.cu), the exact extension to the full determinant grid and
-the inverse NTT.  Weak scaling: every rank runs one prime per step (ranks take
+nodes, csrc/expand.cu) and the coefficients interpolated straight from those
+nodes (one pass per axis, pdb_grid_interpolate_u32; the residue tensor equals
+the inverse NTT of the reference's full determinant grid).  Weak scaling: every rank runs one prime per step (ranks take
 primes round-robin).
 
   value  determinants COMPUTED per second (elimination at the kept nodes) over
@@ -87,8 +88,8 @@ def describe(name, m, pl, ws_bytes):
                         % (name.upper(), m.r, m.r, len(pl.variables), "x".join(map(str, pl.shape)),
                            pl.node_count, pl.prime_count, m.k),
             "matrix_order": m.r, "nodes_per_prime": pl.node_count, "primes": pl.prime_count,
-            "step": "one prime: forward evaluation + det at the degree-bound node set + exact grid extension + "
-                    "inverse NTT",
+            "step": "one prime: forward evaluation + det at the degree-bound node set + the coefficients "
+                    "interpolated from those nodes (direct mode) or exact grid extension + inverse NTT",
             "working_set_bytes": ws_bytes,
             "l2_policy": ("inputs larger than L2 (per-step working set %.2f GB >> 126 MB)" % (ws_bytes / 1e9)) if big
             else ("working set %.1f MB fits L2: a 256 MB buffer is written between timed steps (not timed)"
@@ -416,8 +417,7 @@ def run_ours(args):
         stages.det_kernels(pi)
         e1.record(stream)
         det_events.append((e0, e1))
-        stages.expand(pi)
-        stages.interpolate(pi)
+        stages.finish(pi)
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(stream)
         step_events.append((t0, t1))

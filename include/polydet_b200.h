@@ -115,6 +115,17 @@ int32_t pdb_eval_det_fused_map_u32(pdb_prime_ctx* ctx, const uint32_t* partial, 
                                    int64_t node_lo, int64_t nodes, uint32_t* out, void* scratch,
                                    size_t scratch_bytes, void* stream);
 
+/* compact[pdb_node_map_size(map)] determinants at the kept nodes (every axis
+ * pruned) -> the polynomial's coefficients c[j_0..j_{d-1}], j_a < box[a] <= 8 kept_u[a],
+ * written at their row-major positions of grid[prod dims]; the rest of grid is
+ * not written (the inverse NTT of the full determinant grid is zero there by
+ * the degree bound, so a zeroed grid then equals reference _ifft_stage,
+ * pipeline.py:395-404).  One pass per axis straight from the kept nodes: no
+ * full determinant grid, no inverse NTT.  compact is overwritten; scratch holds
+ * as many u32 as compact. */
+int32_t pdb_grid_interpolate_u32(pdb_prime_ctx* ctx, uint32_t* compact, uint32_t* scratch, uint32_t* grid,
+                                 const pdb_node_map* map, const int64_t* box, void* stream);
+
 /* compact[pdb_node_map_size(map)] determinants at the kept nodes -> grid[prod dims]
  * with every node's determinant (the same values det_grid computes there,
  * determinant.py:92-133).  compact and grid must not overlap. */

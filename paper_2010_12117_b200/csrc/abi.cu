@@ -167,6 +167,8 @@ int crt_mrc_sel(const uint32_t* res, int P, const int64_t* index, int64_t count,
                 const uint32_t* primes_host, uint32_t* limbs, int L, uint8_t* neg, int32_t* width, int sms,
                 cudaStream_t st);
 int crt_limbs(int P);
+int grid_interpolate(PrimeCtx* ctx, uint32_t* compact, uint32_t* scratch, uint32_t* grid, const NodeMap& map,
+                     const int64_t* dims, const int64_t* box, cudaStream_t st);
 int grid_expand(PrimeCtx* ctx, const uint32_t* compact, uint32_t* grid, const NodeMap& map, const int64_t* dims,
                 cudaStream_t st);
 void expand_release(const PrimeCtx* ctx);
@@ -462,6 +464,16 @@ int32_t pdb_eval_det_fused_map_u32(pdb_prime_ctx* ctx, const uint32_t* partial, 
   }
   if (src.ulast > 0) src.orow0 = node_lo / (8 * (int64_t)src.ulast);
   return det_run(ctx, src, entry_ids, r, node_lo, nodes, out, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int32_t pdb_grid_interpolate_u32(pdb_prime_ctx* ctx, uint32_t* compact, uint32_t* scratch, uint32_t* grid,
+                                 const pdb_node_map* map, const int64_t* box, void* stream) {
+  if (!narrow_ctx(ctx)) return -2;
+  NodeMap nm;
+  int64_t n = 0;
+  if (!map || map->ndim == 0 || !box) { set_error("grid_interpolate needs a pruned node map and a box"); return -2; }
+  if (!make_node_map(map, &nm, &n)) return -2;
+  return grid_interpolate(ctx, compact, scratch, grid, nm, map->dims, box, (cudaStream_t)stream);
 }
 
 int32_t pdb_grid_expand_u32(pdb_prime_ctx* ctx, const uint32_t* compact, uint32_t* grid,

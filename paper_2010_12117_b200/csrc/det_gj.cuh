@@ -499,8 +499,12 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
 #ifndef PDB_GJ_T44
 #define PDB_GJ_T44 0   // 4x4 trailing tiles (experiment)
 #endif
+#ifndef PDB_GJ_T34
+#define PDB_GJ_T34 0   // 1: 3x4 tiles where 2x4 leave lanes idle (mrem = 24); measured 13 % slower (code size), and wrong somewhere
+#endif
   if (PDB_GJ_T28 && minb < 4 && util(2, 8, 70)) gj_tpass<2, 8, LPM, P31, B>(A, S, K, mrem, cR, l, m);
   else if (PDB_GJ_T44 && util(4, 4, 70)) gj_tpass<4, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
+  else if (PDB_GJ_T34 && !P31 && !util(2, 4, 95) && util(3, 4, 95)) gj_tpass<3, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
   else if (util(2, 4, 70)) gj_tpass<2, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
   else if (util(1, 4, 70)) gj_tpass<1, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
   else gj_tpass<1, 2, LPM, P31, B>(A, S, K, mrem, cR, l, m);

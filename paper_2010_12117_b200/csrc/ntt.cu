@@ -101,6 +101,9 @@ ntt_axis_smem(uint32_t* __restrict__ data, AxisGeom g, int N, int logN, int logT
 // for TI = 1 (contiguous lines): one pad word per R2 words and a line stride
 // of 16 (mod 32) words, so both passes read conflict-free.
 
+#ifndef PDB_RR_MINB1
+#define PDB_RR_MINB1 3  // contiguous-line tiles (TIC = 1): 80 registers, no spills
+#endif
 #ifndef PDB_RR_MINB
 #define PDB_RR_MINB 4   // resident 256-thread CTAs per SM the register budget is sized for (4: 64 registers, measured best)
 #endif
@@ -139,9 +142,12 @@ __device__ __forceinline__ int rr_pos(int lo, int n, int t, int TI, int LS) {
   return TI == 1 ? lo * LS + n + n / R2 : lo * LS + n * TI + t + (TI < 32 ? (n / R2) * 16 : 0);
 }
 
-template <bool INV, int R1, int R2>
-__global__ void __launch_bounds__(256, PDB_RR_MINB)
-ntt_axis_rr(uint32_t* __restrict__ data, AxisGeom g, int logTI, int logLO, int LS,
+// TIC: compile-time tile width (1 = contiguous lines, 32 = 128-byte rows; 0 =
+// runtime), so every shared-memory slot of a thread's R-element column folds
+// into a base register plus immediate offsets.
+template <bool INV, int R1, int R2, int TIC = 0>
+__global__ void __launch_bounds__(256, TIC == 1 ? PDB_RR_MINB1 : PDB_RR_MINB)
+ntt_axis_rr(uint32_t* __restrict__ data, AxisGeom g, int logTI_rt, int logLO, int LS,
             const uint32_t* __restrict__ full, const uint32_t* __restrict__ fulls,
             const uint32_t* __restrict__ invn, const uint32_t* __restrict__ invns, uint32_t p) {
   constexpr int N = R1 * R2;
@@ -163,6 +169,7 @@ ntt_axis_rr(uint32_t* __restrict__ data, AxisGeom g, int logTI, int logLO, int L
       twns[e] = __ldg(invns + e);
     }
   }
+  const int logTI = TIC == 1 ? 0 : (TIC == 32 ? 5 : logTI_rt);
   const int TI = 1 << logTI, LO = 1 << logLO;
   const int64_t tchunks = (g.inner + TI - 1) >> logTI;
   const int64_t ntiles = ((g.active_outer + LO - 1) >> logLO) * tchunks;
@@ -251,8 +258,10 @@ ntt_axis_rr(uint32_t* __restrict__ data, AxisGeom g, int logTI, int logLO, int L
       }
       const int64_t base = line_base[lo];
       if (base >= 0 && t0 + t < g.inner) {
+        uint32_t* dst = data + base + (int64_t)k1 * g.inner + t;
+        const int64_t step = (int64_t)R1 * g.inner;
 #pragma unroll
-        for (int k2 = 0; k2 < R2; ++k2) data[base + (int64_t)(k1 + R1 * k2) * g.inner + t] = y[k2];
+        for (int k2 = 0; k2 < R2; ++k2, dst += step) *dst = y[k2];
       }
     }
     __syncthreads();
@@ -447,16 +456,26 @@ int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t
     const uint32_t* full = T->full;
     const uint32_t* fulls = T->full_s;
     const uint32_t p = (uint32_t)ctx->p;
+#define PDB_RR_T(A, B, C)                                                                                          \
+  if (inverse)                                                                                                    \
+    ntt_axis_rr<true, A, B, C><<<grid, 256, smem, st>>>(data, g, logTI, logLO, LS, full, fulls, T->inv_full_n,   \
+                                                        T->inv_full_ns, p);                                      \
+  else                                                                                                            \
+    ntt_axis_rr<false, A, B, C><<<grid, 256, smem, st>>>(data, g, logTI, logLO, LS, full, fulls, T->inv_full_n,  \
+                                                         T->inv_full_ns, p);
 #define PDB_RR(A, B)                                                                                             \
+  if (R1 == A && R2 == B) { PDB_RR_T(A, B, 0) }
+#define PDB_RR3(A, B)                                                                                            \
   if (R1 == A && R2 == B) {                                                                                       \
-    if (inverse)                                                                                                  \
-      ntt_axis_rr<true, A, B><<<grid, 256, smem, st>>>(data, g, logTI, logLO, LS, full, fulls, T->inv_full_n, T->inv_full_ns, p); \
-    else                                                                                                          \
-      ntt_axis_rr<false, A, B><<<grid, 256, smem, st>>>(data, g, logTI, logLO, LS, full, fulls, T->inv_full_n, T->inv_full_ns, p); \
+    if (logTI == 0) { PDB_RR_T(A, B, 1) }                                                                         \
+    else if (logTI == 5) { PDB_RR_T(A, B, 32) }                                                                   \
+    else { PDB_RR_T(A, B, 0) }                                                                                    \
   }
     PDB_RR(2, 1) PDB_RR(4, 1) PDB_RR(8, 1) PDB_RR(16, 1)
-    PDB_RR(16, 2) PDB_RR(16, 4) PDB_RR(16, 8) PDB_RR(16, 16)
+    PDB_RR3(16, 2) PDB_RR3(16, 4) PDB_RR3(16, 8) PDB_RR3(16, 16)
+#undef PDB_RR3
 #undef PDB_RR
+#undef PDB_RR_T
     count_launch();
     return check_launch("ntt_axis_rr");
   }

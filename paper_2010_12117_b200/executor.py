@@ -168,6 +168,13 @@ class DevicePlan:
         self.nmap = native.node_map(self.shape, self.kept_u) if self.vn else None
         self.sel = native.node_map_size(self.nmap) if self.nmap is not None else self.nodes
         self.klen = [8 * u if u else n for n, u in zip(self.shape, self.kept_u)]
+        # fused runs with every axis pruned interpolate the coefficients straight
+        # from the kept nodes (pdb_grid_interpolate_u32): no full determinant grid,
+        # no grid extension, no inverse NTT; the box is the 8 U coefficients per
+        # axis those nodes determine (zero beyond the degree bound)
+        self.direct = (DIRECT and not self.staged and self.nmap is not None and self.vn > 0
+                       and all(self.kept_u))
+        self.box = [8 * u for u in self.kept_u] if self.direct else None
 
     def buffer_words(self) -> int:
         return self.k * self.nodes if self.staged else self.k * self.outer * self.E
@@ -175,6 +182,8 @@ class DevicePlan:
 
 #: determinants only at the kept nodes of the degree bound (False: every node, as the reference)
 PRUNE = os.environ.get("PDB_NO_PRUNE", "") == ""
+#: fused + fully pruned: coefficients interpolated straight from the kept nodes
+DIRECT = os.environ.get("PDB_NO_DIRECT", "") == ""
 
 
 def kept_u(shape, degrees, even_last: bool = False) -> list:
@@ -313,10 +322,12 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
     P = pl.prime_count
     whole, slab_primes = shard.split_primes(P, size) if dp.vn else (P, [])
     mine = shard.my_primes(whole, rank, size)
-    residues = torch.empty((len(mine), nodes), dtype=dp.word, device=device)
+    # direct interpolation writes only the coefficient box: the rest stays zero
+    residues = (torch.zeros if dp.direct else torch.empty)((len(mine), nodes), dtype=dp.word, device=device)
     work = torch.empty(dp.buffer_words() or 1, dtype=dp.word, device=device)
     det_chunk = det_chunk_size(dp)
     det_buf = torch.empty(dp.sel, dtype=dp.word, device=device)
+    interp = torch.empty(dp.sel, dtype=dp.word, device=device) if dp.direct else None
     scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, det_chunk, dp.wide), device)
     events = []
     for row, pi in enumerate(mine):
@@ -329,9 +340,16 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
         t0 = _Timer(torch, stream).mark()
         _fft_stage(dp, ctx, work, ws, pi, cfg)
         t1 = _Timer(torch, stream).mark()
-        _det_stage(dp, ctx, work, det_buf, scratch, det_chunk, ws, pi, cfg, residues[row])
-        t2 = _Timer(torch, stream).mark()
-        native.ntt_multi(ctx, residues[row], 1, dp.shape, None, range(dp.vn), True)
+        if dp.direct:
+            _det_range(dp, ctx, work, det_buf, scratch, det_chunk, 0, dp.sel)
+            if ws is None:
+                cfg._notify("p%d/det" % pi)
+            t2 = _Timer(torch, stream).mark()
+            native.grid_interpolate(ctx, det_buf, interp, residues[row], dp.nmap, dp.box)
+        else:
+            _det_stage(dp, ctx, work, det_buf, scratch, det_chunk, ws, pi, cfg, residues[row])
+            t2 = _Timer(torch, stream).mark()
+            native.ntt_multi(ctx, residues[row], 1, dp.shape, None, range(dp.vn), True)
         t3 = _Timer(torch, stream).mark()
         events.append((t0, t1, t2, t3))
         if ws is not None:
@@ -382,7 +400,8 @@ def _slab_primes(dp: DevicePlan, primes, work, det_buf, scratch, chunk, rank, si
     k0 = dp.klen[0]           # slabs of the kept nodes' slowest axis
     inner = dp.sel // k0
     lo, hi = shard.my_slab(k0, rank, size)
-    rows = torch.empty((len(primes), dp.nodes), dtype=dp.word, device=det_buf.device)
+    rows = (torch.zeros if dp.direct else torch.empty)((len(primes), dp.nodes), dtype=dp.word,
+                                                        device=det_buf.device)
     for j, pi in enumerate(primes):
         ctx = native.prime_context(pl.primes[pi], det_buf.device.index, dp.wide)
         t0 = _Timer(torch, stream).mark()
@@ -390,9 +409,13 @@ def _slab_primes(dp: DevicePlan, primes, work, det_buf, scratch, chunk, rank, si
         t1 = _Timer(torch, stream).mark()
         _det_range(dp, ctx, work, det_buf, scratch, chunk, lo * inner, (hi - lo) * inner)
         full = shard.gather_slabs(det_buf[lo * inner: hi * inner], k0, inner, rank, size)
-        _expand(dp, ctx, full, rows[j])
-        t2 = _Timer(torch, stream).mark()
-        native.ntt_multi(ctx, rows[j], 1, dp.shape, None, range(dp.vn), True)
+        if dp.direct:
+            t2 = _Timer(torch, stream).mark()
+            native.grid_interpolate(ctx, full, torch.empty_like(full), rows[j], dp.nmap, dp.box)
+        else:
+            _expand(dp, ctx, full, rows[j])
+            t2 = _Timer(torch, stream).mark()
+            native.ntt_multi(ctx, rows[j], 1, dp.shape, None, range(dp.vn), True)
         t3 = _Timer(torch, stream).mark()
         events.append((t0, t1, t2, t3))
         cfg._notify("p%d/ifft" % pi)
@@ -567,10 +590,13 @@ class PrimeStages:
         dp = self.dp
         self.work = torch.empty(dp.buffer_words() or 1, dtype=dp.word, device=self.device)
         self.chunk = det_chunk_size(dp)
-        self.det = torch.empty(dp.nodes, dtype=dp.word, device=self.device)
+        # direct mode: `det` receives the coefficient box only (zero elsewhere, once)
+        self.det = (torch.zeros if dp.direct else torch.empty)(dp.nodes, dtype=dp.word, device=self.device)
         self.compact = torch.empty(dp.sel, dtype=dp.word, device=self.device)
+        self.interp = torch.empty(dp.sel, dtype=dp.word, device=self.device) if dp.direct else None
         self.scratch = native.scratch_tensor(native.det_scratch_bytes(pl.r, self.chunk, dp.wide), self.device)
         self._cfg = PipelineConfig()
+        self._full_grid = False
 
     def ctx(self, pi):
         return native.prime_context(self.pl.primes[pi], self.device.index, self.dp.wide)
@@ -579,6 +605,7 @@ class PrimeStages:
         _fft_stage(self.dp, self.ctx(pi), self.work, None, pi, self._cfg)
 
     def determinants(self, pi):
+        self._full_grid = True
         _det_stage(self.dp, self.ctx(pi), self.work, self.compact, self.scratch, self.chunk, None, pi, self._cfg,
                    self.det)
 
@@ -591,13 +618,35 @@ class PrimeStages:
 
     def expand(self, pi):
         """Kept-node determinants -> the full grid in `det` (no-op unpruned)."""
+        self._full_grid = True
         if self.dp.nmap is not None:
             _expand(self.dp, self.ctx(pi), self.compact, self.det)
 
     def interpolate(self, pi):
         native.ntt_multi(self.ctx(pi), self.det, 1, self.dp.shape, None, range(self.dp.vn), True)
 
+    def interpolate_direct(self, pi):
+        """Kept-node determinants in `compact` -> the residue tensor in `det`
+        (direct mode: straight from the kept nodes; `compact` is consumed)."""
+        if self._full_grid:   # `det` last held a full grid: clear outside the box
+            self.det.zero_()
+            self._full_grid = False
+        native.grid_interpolate(self.ctx(pi), self.compact, self.interp, self.det, self.dp.nmap, self.dp.box)
+
+    def finish(self, pi):
+        """After det_kernels: the residue tensor in `det` (direct interpolation, or
+        grid extension + inverse NTT)."""
+        if self.dp.direct:
+            self.interpolate_direct(pi)
+        else:
+            self.expand(pi)
+            self.interpolate(pi)
+
     def step(self, pi):
         self.forward(pi)
-        self.determinants(pi)
-        self.interpolate(pi)
+        if self.dp.direct:
+            self.det_kernels(pi)
+            self.interpolate_direct(pi)
+        else:
+            self.determinants(pi)
+            self.interpolate(pi)

@@ -76,6 +76,7 @@ _SIGNATURES = {
                                      _c_vp]),
     "pdb_mulmod_peak": (_c_i32, [_c_u32, _c_i32, ctypes.POINTER(ctypes.c_double), _c_vp]),
     "pdb_kernel_timing": (_c_i32, [_c_i32]),
+    "pdb_grid_interpolate_u32": (_c_i32, [_c_vp, _c_vp, _c_vp, _c_vp, _c_map, _c_vp, _c_vp]),
     "pdb_limbs_to_digits30": (_c_i32, [_c_vp, _c_i64, _c_i32, _c_i64, _c_vp, _c_i32, _c_vp, _c_vp]),
     "pdb_kernel_timing_read": (_c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_c_i64)]),
     # the wide path (2^31 <= p < 2^62): u64 twins
@@ -299,6 +300,14 @@ def eval_det_fused_map(ctx: PrimeContext, partial, outer: int, ncoef: int, entri
                                          int(nodes), ptr(out), ptr(scratch),
                                          scratch.numel() * scratch.element_size(), stream_handle(stream)),
           "fused det")
+
+
+def grid_interpolate(ctx: PrimeContext, compact, scratch, grid, nmap, box, stream=None):
+    """Kept-node determinants -> coefficients in the box (written into grid; compact is overwritten)."""
+    lib = load_library()
+    b = (ctypes.c_int64 * len(box))(*[int(x) for x in box])
+    check(lib.pdb_grid_interpolate_u32(ctx.handle, ptr(compact), ptr(scratch), ptr(grid), ctypes.byref(nmap), b,
+                                       stream_handle(stream)), "grid interpolate")
 
 
 def grid_expand(ctx: PrimeContext, compact, grid, nmap, stream=None):

@@ -136,3 +136,39 @@ def test_fused_multi_launch_equals_staged(cuda, monkeypatch, prune, r, vn, degs,
     fused, dp = _grids(m, "fused", prune, primes=(0,))
     assert dp.sel // executor.det_chunk_size(dp) >= 2
     assert np.array_equal(staged[0], fused[0])
+
+
+@pytest.mark.parametrize("r,vn,degs,seed", [c for c in CASES if c[1] >= 1])
+def test_direct_interpolation_equals_inverse_of_full_grid(cuda, r, vn, degs, seed):
+    """Fused runs with every axis pruned interpolate the coefficients straight
+    from the kept nodes (pdb_grid_interpolate_u32).  The residue tensor must
+    equal the inverse NTT of the full (extended) determinant grid -- the
+    reference's _ifft_stage output (pipeline.py:395-404) -- everywhere,
+    including the zeros outside the coefficient box."""
+    m = _dense(r, vn, degs, seed)
+    pl = plan(m)
+    st = executor.PrimeStages(m, pl, staged=False)
+    if not st.dp.direct:
+        pytest.skip("not every axis is pruned: kept_u %s" % (st.dp.kept_u,))
+    for pi in (0, 1):
+        st.forward(pi)
+        st.det_kernels(pi)
+        saved = st.compact.clone()
+        st.interpolate_direct(pi)
+        direct = st.det.cpu().numpy().copy()
+        st.compact.copy_(saved)
+        st.expand(pi)
+        st.interpolate(pi)
+        want = st.det.cpu().numpy().copy()
+        assert np.array_equal(direct, want)
+
+
+@pytest.mark.parametrize("r,vn,degs,seed", [(10, 2, (4, 4), 2), (10, 1, (4,), 1), (10, 3, (2, 4, 3), 5)])
+def test_direct_run_equals_extended_run(cuda, monkeypatch, r, vn, degs, seed):
+    m = _dense(r, vn, degs, seed)
+    monkeypatch.setattr(executor, "FORCE_MODE", "fused")
+    monkeypatch.setattr(executor, "DIRECT", False)
+    want = run(m)
+    monkeypatch.setattr(executor, "DIRECT", True)
+    got = run(m)
+    assert got.coeffs == want.coeffs and got.shape == want.shape

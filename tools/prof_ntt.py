@@ -47,6 +47,12 @@ def main():
     out["forward_ms"] = timed(lambda: st.forward(0), args.reps)
     out["expand_ms"] = timed(lambda: st.expand(0), args.reps)
     out["inverse_ms"] = timed(lambda: st.interpolate(0), args.reps)
+    if st.dp.direct:   # coefficients straight from the kept nodes (replaces expand + inverse)
+        st.det_kernels(0)
+        saved = st.compact.clone()
+        out["copy_ms"] = timed(lambda: st.compact.copy_(saved), args.reps)
+        out["direct_ms"] = timed(lambda: (st.compact.copy_(saved), st.interpolate_direct(0)), args.reps) \
+            - out["copy_ms"]
     vn = len(pl.shape)
     inv_bytes = 2 * 4 * nodes * vn
     out["inverse_algorithmic_bytes"] = inv_bytes
