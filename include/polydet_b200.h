@@ -62,6 +62,15 @@ int32_t pdb_ntt_multi_u32(pdb_prime_ctx* ctx, uint32_t* data, int64_t batch, int
                           const int64_t* dims, const int64_t* extents, uint32_t axis_mask,
                           int32_t inverse, void* stream);
 
+/* Forward transform for a pruned node set (executor.kept_u): as pdb_ntt_multi_u32
+ * (forward), except that an axis with kept_u[a] > 0 (N_a >= 16, 8 kept_u[a] < N_a)
+ * evaluates only its nodes u + (N_a/8) v, u < kept_u[a], and passes skip the
+ * lines of non-kept nodes of the next axis.  Positions of non-kept nodes are
+ * left unwritten: only the fused determinant of the kept nodes reads the result. */
+int32_t pdb_ntt_forward_kept_u32(pdb_prime_ctx* ctx, uint32_t* data, int64_t batch, int32_t ndim,
+                                 const int64_t* dims, const int64_t* extents, const int64_t* kept_u,
+                                 uint32_t axis_mask, void* stream);
+
 /* dst[pos[i]] = (sign_i * sum_l mag[i*limbs + l] 2^(32 l)) mod p. */
 int32_t pdb_reduce_scatter_u32(pdb_prime_ctx* ctx, const uint32_t* mag, const uint8_t* neg,
                                const int64_t* pos, int64_t count, int32_t limbs, uint32_t* dst,

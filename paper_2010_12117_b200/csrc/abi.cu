@@ -383,6 +383,28 @@ int32_t pdb_ntt_multi_u32(pdb_prime_ctx* ctx, uint32_t* data, int64_t batch, int
   return 0;
 }
 
+int32_t pdb_ntt_forward_kept_u32(pdb_prime_ctx* ctx, uint32_t* data, int64_t batch, int32_t ndim,
+                                 const int64_t* dims, const int64_t* extents, const int64_t* kept_u,
+                                 uint32_t axis_mask, void* stream) {
+  if (!narrow_ctx(ctx)) return -2;
+  if (ndim < 0 || ndim > PDB_MAX_DIMS || batch < 0 || !kept_u) { set_error("invalid NTT arguments"); return -2; }
+  for (int a = 0; a < ndim; ++a) {
+    if (kept_u[a] < 0 || (kept_u[a] > 0 && (dims[a] < 16 || 8 * kept_u[a] >= dims[a]))) {
+      set_error("kept u %lld invalid for axis %d of length %lld", (long long)kept_u[a], a, (long long)dims[a]);
+      return -2;
+    }
+    if ((axis_mask >> a) & 1)
+      if (!ctx_twiddles(ctx, (int)dims[a])) return -2;
+  }
+  if (batch == 0) return 0;
+  for (int a = ndim - 1; a >= 0; --a) {
+    if (!((axis_mask >> a) & 1)) continue;
+    int rc = ntt_axis(ctx, data, batch, ndim, dims, extents, a, false, (cudaStream_t)stream, kept_u);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
 int32_t pdb_reduce_scatter_u32(pdb_prime_ctx* ctx, const uint32_t* mag, const uint8_t* neg,
                                const int64_t* pos, int64_t count, int32_t limbs, uint32_t* dst,
                                void* stream) {

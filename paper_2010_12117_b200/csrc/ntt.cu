@@ -325,23 +325,28 @@ __global__ void ntt_stage_global(uint32_t* __restrict__ data, AxisGeom g, int N,
 // threads split the N/8 values of u of one tile of TI columns; the E rows are
 // read before any output of the tile is written (all writers of rows < E of
 // these columns are in this CTA, __syncthreads in between).
+// Pruned node sets (executor.kept_u): ukeep > 0 computes only the outputs
+// u + (N/8) v with u < ukeep; tiles whose first inner index (the next axis,
+// already evaluated, stride kdiv words) is not a kept node of that axis
+// (u' = index mod kn8 >= ku) are skipped -- no determinant reads them.
 template <int E, int V>
 __global__ void __launch_bounds__(256)
 ntt_axis_sparse(uint32_t* __restrict__ data, AxisGeom g, int N, int TI, const uint32_t* __restrict__ full,
-                const uint32_t* __restrict__ fulls, uint32_t p) {
-  const int N8 = N / 8;
+                const uint32_t* __restrict__ fulls, uint32_t p, int ukeep, int64_t kdiv, int kn8, int ku) {
+  const int N8 = ukeep > 0 ? ukeep : N / 8;
   const int64_t tchunks = (g.inner + TI - 1) / TI;
   const int64_t ntiles = g.active_outer * tchunks;
   uint32_t w[4], ws[4];
   w[0] = ws[0] = 0;
 #pragma unroll
-  for (int v = 1; v < 4; ++v) { w[v] = __ldg(full + v * N8); ws[v] = __ldg(fulls + v * N8); }
+  for (int v = 1; v < 4; ++v) { w[v] = __ldg(full + v * (N / 8)); ws[v] = __ldg(fulls + v * (N / 8)); }
   const int cols = TI / V;                       // column groups per tile
   const int cg = threadIdx.x % cols;
   const int ug = threadIdx.x / cols, ugs = blockDim.x / cols;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t oc = tile / tchunks;
     const int64_t t0 = (tile - oc * tchunks) * TI + (int64_t)cg * V;
+    if (ku > 0 && (int)((((tile - oc * tchunks) * TI) / kdiv) % kn8) >= ku) continue;   // uniform per tile
     const int64_t base = outer_offset(oc, g) * (int64_t)N * g.inner + t0;
     const bool live = t0 < g.inner && ug < ugs;   // V | inner on the vector path
     uint32_t c[V][E];
@@ -372,7 +377,7 @@ ntt_axis_sparse(uint32_t* __restrict__ data, AxisGeom g, int N, int TI, const ui
         for (int q = 0; q < V; ++q) gj_dft8<E>(c[q], tw, tws, w, ws, p, x[q]);
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
-          uint32_t* o = data + base + (int64_t)(u + v * N8) * g.inner;
+          uint32_t* o = data + base + (int64_t)(u + v * (N / 8)) * g.inner;
           if constexpr (V == 4) *reinterpret_cast<uint4*>(o) = make_uint4(x[0][v], x[1][v], x[2][v], x[3][v]);
           else *o = x[0][v];
         }
@@ -386,7 +391,7 @@ ntt_axis_sparse(uint32_t* __restrict__ data, AxisGeom g, int N, int TI, const ui
 // ext (may be null) gives, per dim, how many leading indices can be nonzero
 // on the dims before `axis` (lines outside that box are skipped).
 int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t* dims,
-             const int64_t* ext, int axis, bool inverse, cudaStream_t st) {
+             const int64_t* ext, int axis, bool inverse, cudaStream_t st, const int64_t* kept) {
   const int N = (int)dims[axis];
   if (N == 1) return 0;  // length-1 transform is the identity (inverse scale 1)
   const Twiddles* T = ctx_twiddles(ctx, N);
@@ -420,10 +425,20 @@ int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t
     const int64_t tiles = g.active_outer * ((g.inner + TI - 1) / TI);
     const int grid = (int)(tiles < (int64_t)ctx->sms * 16 ? tiles : (int64_t)ctx->sms * 16);
     const uint32_t p = (uint32_t)ctx->p;
+    // kept node sets: outputs u < kept[axis]; tiles of non-kept next-axis nodes skipped
+    const int ukeep = kept && kept[axis] > 0 ? (int)kept[axis] : 0;
+    int64_t kdiv = 1;
+    int kn8 = 1, ku = 0;
+    if (kept && axis + 1 < nd && kept[axis + 1] > 0 && dims[axis + 1] >= 16) {
+      for (int d = axis + 2; d < nd; ++d) kdiv *= dims[d];
+      kn8 = (int)(dims[axis + 1] / 8);
+      ku = (int)kept[axis + 1];
+      if (kdiv % TI) ku = 0;   // a tile must not straddle two next-axis nodes
+    }
     switch (E * 2 + (vec ? 1 : 0)) {
 #define PDB_SPARSE(EE)                                                                                        \
-  case EE * 2: ntt_axis_sparse<EE, 1><<<grid, threads, 0, st>>>(data, g, N, TI, T->full, T->full_s, p); break; \
-  case EE * 2 + 1: ntt_axis_sparse<EE, 4><<<grid, threads, 0, st>>>(data, g, N, TI, T->full, T->full_s, p); break;
+  case EE * 2: ntt_axis_sparse<EE, 1><<<grid, threads, 0, st>>>(data, g, N, TI, T->full, T->full_s, p, ukeep, kdiv, kn8, ku); break; \
+  case EE * 2 + 1: ntt_axis_sparse<EE, 4><<<grid, threads, 0, st>>>(data, g, N, TI, T->full, T->full_s, p, ukeep, kdiv, kn8, ku); break;
       PDB_SPARSE(1) PDB_SPARSE(2) PDB_SPARSE(3) PDB_SPARSE(4)
       PDB_SPARSE(5) PDB_SPARSE(6) PDB_SPARSE(7) PDB_SPARSE(8)
 #undef PDB_SPARSE

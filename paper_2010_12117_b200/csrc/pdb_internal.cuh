@@ -88,8 +88,10 @@ void count_launch(long long n = 1);
 int ktimer_start(cudaStream_t st);
 void ktimer_stop(int slot, cudaStream_t st);
 
+// kept (may be null): per axis, evaluate only the kept nodes u < kept[a] of a
+// pruned node set (forward sparse passes; the other outputs are not written)
 int ntt_axis(PrimeCtx* ctx, uint32_t* data, int64_t batch, int nd, const int64_t* dims,
-             const int64_t* ext, int axis, bool inverse, cudaStream_t st);
+             const int64_t* ext, int axis, bool inverse, cudaStream_t st, const int64_t* kept = nullptr);
 
 // ---- pruned node sets ----------------------------------------------------------
 // The determinant is a polynomial of degree <= D_a in variable a (the plan's

@@ -182,6 +182,8 @@ class DevicePlan:
 
 #: determinants only at the kept nodes of the degree bound (False: every node, as the reference)
 PRUNE = os.environ.get("PDB_NO_PRUNE", "") == ""
+#: fused + pruned: the forward passes evaluate only the kept nodes of the leading axes
+FORWARD_KEPT = os.environ.get("PDB_NO_FORWARD_KEPT", "") == ""
 #: fused + fully pruned: coefficients interpolated straight from the kept nodes
 DIRECT = os.environ.get("PDB_NO_DIRECT", "") == ""
 
@@ -491,7 +493,11 @@ def _fft_stage(dp: DevicePlan, ctx, work, ws, pi, cfg):
         else:
             work.zero_()
         native.reduce_scatter(ctx, dp.mag, dp.neg, dp.pos, dp.count, dp.L, work)
-        native.ntt_multi(ctx, work, 1, dims, ext, range(dp.vn - 1), False)
+        if dp.nmap is not None and FORWARD_KEPT and _sparse_leading_axes(dp):
+            # pruned node set: evaluate the leading axes at their kept nodes only
+            native.ntt_forward_kept(ctx, work, 1, dims, ext, list(dp.kept_u[:-1]) + [0, 0], range(dp.vn - 1))
+        else:
+            native.ntt_multi(ctx, work, 1, dims, ext, range(dp.vn - 1), False)
         if ws is None:
             # progress only: fused mode stores no fft/det artifacts, so with a
             # workspace it reports (and checkpoints) p{i}/ifft units alone

@@ -76,6 +76,7 @@ _SIGNATURES = {
                                      _c_vp]),
     "pdb_mulmod_peak": (_c_i32, [_c_u32, _c_i32, ctypes.POINTER(ctypes.c_double), _c_vp]),
     "pdb_kernel_timing": (_c_i32, [_c_i32]),
+    "pdb_ntt_forward_kept_u32": (_c_i32, [_c_vp, _c_vp, _c_i64, _c_i32, _c_vp, _c_vp, _c_vp, _c_u32, _c_vp]),
     "pdb_grid_interpolate_u32": (_c_i32, [_c_vp, _c_vp, _c_vp, _c_vp, _c_map, _c_vp, _c_vp]),
     "pdb_limbs_to_digits30": (_c_i32, [_c_vp, _c_i64, _c_i32, _c_i64, _c_vp, _c_i32, _c_vp, _c_vp]),
     "pdb_kernel_timing_read": (_c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_c_i64)]),
@@ -228,6 +229,17 @@ def ntt_multi(ctx: PrimeContext, data, batch: int, dims, extents, axes, inverse:
     fn = lib.pdb_ntt_multi_u64 if ctx.wide else lib.pdb_ntt_multi_u32
     check(fn(ctx.handle, ptr(data), int(batch), nd, host_i64(dims), ext, mask, int(bool(inverse)),
              stream_handle(stream)), "ntt")
+
+
+def ntt_forward_kept(ctx: PrimeContext, data, batch: int, dims, extents, kept_u, axes, stream=None):
+    """Forward NTT evaluating only the kept nodes of a pruned node set (u32 path)."""
+    lib = load_library()
+    mask = 0
+    for a in axes:
+        mask |= 1 << a
+    ext = host_i64(extents) if extents is not None else None
+    check(lib.pdb_ntt_forward_kept_u32(ctx.handle, ptr(data), int(batch), len(dims), host_i64(dims), ext,
+                                       host_i64(kept_u), mask, stream_handle(stream)), "ntt")
 
 
 def reduce_scatter(ctx: PrimeContext, mag, neg, pos, count: int, limbs: int, dst, stream=None):
