@@ -29,6 +29,19 @@ for r in (16, 40):   # compile-time-order kernels with the dense DFT-8 fill (dis
     rows = [[{(0,): rr.randint(-10**6, 10**6), (1,): rr.randint(-10**6, 10**6)} for _ in range(r)] for _ in range(r)]
     executor.FORCE_MODE = "fused"
     run(poly_matrix(rows, ("x",)))
+# every axis pruned: kept-node forward passes + direct interpolation (grid_interp)
+import itertools  # noqa: E402
+mons = list(itertools.product(range(5), range(5)))
+rows = [[{e: rr.randint(-50, 50) for e in mons if rr.random() < 0.8} for _ in range(10)] for _ in range(10)]
+executor.FORCE_MODE = "fused"
+run(poly_matrix(rows, ("x", "y")))
+# register-radix NTTs on assorted tile shapes (TI = 1, 2..16, 32), forward and inverse
+from paper_2010_12117_b200 import TwiddleTable, encode, ntt_forward_multi, ntt_inverse_multi, reduce_mod  # noqa: E402
+tab = TwiddleTable(spec)
+for shape in [(64,), (16, 16, 8), (256, 4), (32, 2), (128, 64)]:
+    terms = {tuple(rr.randrange(n) for n in shape): rr.randint(1, 10**6) for _ in range(50)}
+    t = reduce_mod(encode(terms, shape, tuple("abc"[:len(shape)])), spec)
+    assert ntt_inverse_multi(ntt_forward_multi(t, tab), tab).residues.tolist() == t.residues.tolist()
 executor.FORCE_MODE = None
 run(*workloads.c1())
 m = workloads.c1()[0]
