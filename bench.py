@@ -486,7 +486,10 @@ def run_ours(args):
     if not args.no_poly:
         del stages, dp
         torch.cuda.empty_cache()
-        poly_e2e_all = poly_e2e(world, rank, cpu=not args.no_cpu_baseline)
+        try:
+            poly_e2e_all = poly_e2e(world, rank, cpu=not args.no_cpu_baseline)
+        except Exception as exc:   # keep the measured line: report the failure in it
+            poly_e2e_all = {"error": "%s: %s" % (type(exc).__name__, exc)}
 
     if rank != 0:
         if world > 1:
