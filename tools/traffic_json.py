@@ -31,7 +31,12 @@ def main():
         v, u = d[k]
         return float(v.replace(",", "")) * UNITS.get(u, 1)
 
-    nodes = 262144
+    # optional: nodes in the profiled launch and nodes per coefficient slab (the
+    # pruned C5 launch covers whole kept last-axis rows of 176 nodes)
+    nodes = int(sys.argv[3]) if len(sys.argv) > 3 else 262144
+    row = int(sys.argv[4]) if len(sys.argv) > 4 else 256
+    slab = 5 * 1600 * 4
+    algo = nodes // row * slab + 8 * nodes
     _, srows = ncu_rows(rep)
     mix = collections.Counter()
     for r in srows:
@@ -42,12 +47,13 @@ def main():
     out = {
         "kernel": "det_gj_kernel<FusedSrc,1,16,P31=0,RPC=40> (C5 prime 0, 40x40, fused DFT-8 fill)",
         "source": "%s (ncu --set full --clock-control none, tools/gpu_prof.sh)" % raw,
-        "command": "python tools/det_bench.py --r '' --nodes 262144 --fused --reps 1",
+        "command": "python tools/det_bench.py --r '' --nodes 262144 %s --reps 1" % ("--pruned" if row != 256 else "--fused"),
         "nodes_per_launch": nodes,
         "dram_read_bytes": val("dram__bytes_read.sum"),
         "dram_write_bytes": val("dram__bytes_write.sum"),
-        "algorithmic_bytes": 34865152,
-        "algorithmic_note": "one [E=5][k=1600] u32 coefficient slab per outer index o (256 nodes), + num/den u32 per node",
+        "algorithmic_bytes": algo,
+        "algorithmic_note": "one [E=5][k=1600] u32 coefficient slab per outer index o (%d nodes of the launch), "
+                            "+ num/den u32 per node" % row,
         "dram_bytes_per_node": (val("dram__bytes_read.sum") + val("dram__bytes_write.sum")) / nodes,
         "duration_s": val("gpu__time_duration.sum"),
         "pipes_pct_of_peak": {
