@@ -499,12 +499,8 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
 #ifndef PDB_GJ_T44
 #define PDB_GJ_T44 0   // 4x4 trailing tiles (experiment)
 #endif
-#ifndef PDB_GJ_T34
-#define PDB_GJ_T34 0   // 1: 3x4 tiles where 2x4 leave lanes idle (mrem = 24); measured 13 % slower (code size), and wrong somewhere
-#endif
   if (PDB_GJ_T28 && minb < 4 && util(2, 8, 70)) gj_tpass<2, 8, LPM, P31, B>(A, S, K, mrem, cR, l, m);
   else if (PDB_GJ_T44 && util(4, 4, 70)) gj_tpass<4, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
-  else if (PDB_GJ_T34 && !P31 && !util(2, 4, 95) && util(3, 4, 95)) gj_tpass<3, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
   else if (util(2, 4, 70)) gj_tpass<2, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
   else if (util(1, 4, 70)) gj_tpass<1, 4, LPM, P31, B>(A, S, K, mrem, cR, l, m);
   else gj_tpass<1, 2, LPM, P31, B>(A, S, K, mrem, cR, l, m);
@@ -584,9 +580,6 @@ __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, in
 // ---- the kernel ------------------------------------------------------------------------------
 #ifndef PDB_GJ_GELAST
 #define PDB_GJ_GELAST 1   // last pivot block: elimination without the Gauss-Jordan back part
-#endif
-#ifndef PDB_GJ_DS
-#define PDB_GJ_DS 0   // 1: pivot pairs by 2x2 Cramer steps (measured ~1 % slower than one pivot per step)
 #endif
 #ifndef PDB_GJ_ABL
 #define PDB_GJ_ABL 0   // profiling ablation only (1: no M pass, 2: no T pass, 3: one fill per CTA); results are wrong
@@ -675,96 +668,6 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         const uint32_t* src_row = A + (K + pj) * S + K + pc;
 #pragma unroll
         for (int k = 0; k < EPL; ++k) v[k] = src_row[k];
-      }
-      if constexpr (PDB_GJ_DS && !P31 && EPL >= 2 && B % 2 == 0) {
-        // Pivot pairs (s, s+1) eliminated at once by the 2x2 Cramer step, all in
-        // the augmented [A11 | E] stored in place (E column s enters as sigma e_s):
-        //   pivot block P = [[a, b], [c, d]], D = det P, sigma = D_0 ... D_{k-1};
-        //   other rows  R_i <- D R_i - alpha_i R_s - beta_i R_{s+1},
-        //               alpha_i = d t_a - c t_b, beta_i = a t_b - b t_a  (t = row i at s, s+1);
-        //   pivot rows  [R_s; R_{s+1}] <- sigma adj(P) [R_s; R_{s+1}].
-        // Every row keeps the common scale sigma, so after B/2 steps the A11 part is
-        // c I with c = prod D_k and the E part is X = c A11^-1 (same contract as
-        // the single-step elimination below); det A11 = prod D_k / prod sigma_k^2.
-        // Per pair: 3 products + one REDC per element (two single steps: 4 + 2).
-        uint32_t sig = one, sprod = one;
-#pragma unroll
-        for (int kp = 0; kp < B / 2; ++kp) {
-          const int s = 2 * kp;
-          const int ks = s % EPL, ls = s / EPL;   // element index / lane-in-row of columns s, s+1
-          const uint32_t a = __shfl_sync(omask, v[ks], s * LPR + ls, LPM);
-          const uint32_t b = __shfl_sync(omask, v[ks + 1], s * LPR + ls, LPM);
-          const uint32_t c = __shfl_sync(omask, v[ks], (s + 1) * LPR + ls, LPM);
-          const uint32_t d = __shfl_sync(omask, v[ks + 1], (s + 1) * LPR + ls, LPM);
-          const uint32_t D = gj_red2(mad_wide(a, d, mad_wide(p - b, c, 0ull)), m);
-          if (kp >= 1) sprod = gj_mont(sprod, sig, m);
-          if (mrem == 0 && kp == B / 2 - 1) {   // last block, last pair: only its D is needed
-            sig = gj_mont(sig, D, m);
-            break;
-          }
-          const uint32_t ta = __shfl_sync(omask, v[ks], pj * LPR + ls, LPM);
-          const uint32_t tb = __shfl_sync(omask, v[ks + 1], pj * LPR + ls, LPM);
-          const bool ps_row = pj == s, ps1_row = pj == s + 1, piv = ps_row || ps1_row;
-          // this lane's half of the row coefficients: nu (even lanes) or rho (odd lanes)
-          uint32_t cf[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (LPR >= 2 && h != ((l % LPR) & 1)) continue;
-            uint32_t m1, n1, m2, n2;
-            if (h == 0) { m1 = piv ? sig : c; n1 = ps_row ? d : (ps1_row ? p - c : tb); m2 = piv ? 0u : p - d; n2 = ta; }
-            else { m1 = piv ? sig : b; n1 = ps_row ? p - b : (ps1_row ? a : ta); m2 = piv ? 0u : p - a; n2 = tb; }
-            cf[h] = gj_red2(mad_wide(m1, n1, mad_wide(m2, n2, 0ull)), m);
-          }
-          uint32_t nu, rho;
-          if constexpr (LPR >= 2) {
-            const bool odd = (l % LPR) & 1;
-            const uint32_t mine = odd ? cf[1] : cf[0];
-            const uint32_t other = __shfl_xor_sync(omask, mine, 1, LPM);
-            nu = odd ? other : mine;
-            rho = odd ? mine : other;
-          } else {
-            nu = cf[0];
-            rho = cf[1];
-          }
-          const uint32_t mu = piv ? 0u : D;
-          const bool inj = (l % LPR) == ls;   // this lane holds columns s, s+1 (E columns enter here)
-#pragma unroll
-          for (int k = 0; k < EPL; ++k) {
-            // last block: only columns > s + 1 feed a later pivot (some lane's column pc + k)
-            if (mrem == 0 && !(B - EPL + k > s + 1)) continue;
-            uint32_t x = v[k];
-            uint32_t y = __shfl_sync(omask, v[k], s * LPR + l % LPR, LPM);
-            uint32_t z = __shfl_sync(omask, v[k], (s + 1) * LPR + l % LPR, LPM);
-            if (k == ks) {
-              x = inj ? (ps_row ? sig : 0u) : x;
-              y = inj ? sig : y;
-              z = inj ? 0u : z;
-            } else if (k == ks + 1) {
-              x = inj ? (ps1_row ? sig : 0u) : x;
-              y = inj ? 0u : y;
-              z = inj ? sig : z;
-            }
-            v[k] = gj_red2(mad_wide(mu, x, mad_wide(nu, y, mad_wide(rho, z, 0ull))), m);
-          }
-          sig = gj_mont(sig, D, m);
-        }
-        if (sig == 0) return false;   // some D_k vanished
-        // det(A11) = c / (sigma_1 ... sigma_{B/2-1})^2; one lane carries the factor
-        den = gj_mont(den, l == 0 ? gj_mont(sprod, sprod, m) : one, m);
-        num = gj_mont(num, sig, m);
-        if (mrem == 0) return true;
-        const uint32_t cR = sig;
-        Q = gj_mont(Q, cR, m);
-        if (K + B < RP - TAIL4) C8 = gj_mont(C8, Q, m);
-        else C4 = gj_mont(C4, Q, m);
-#pragma unroll
-        for (int k = 0; k < EPL; ++k) NX[gj_nx_row(pj) + pc + k] = v[k] ? p - v[k] : 0u;
-        __syncwarp(omask);
-        if (PDB_GJ_ABL != 1) gj_mpass_any<LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
-        __syncwarp(omask);
-        if (PDB_GJ_ABL != 2) gj_tpass_any<LPM, P31, B>(A, S, K, mrem, cR, l, m);
-        __syncwarp(omask);
-        return true;
       }
       uint32_t lam = one, zl = one, zlast = one;
 #pragma unroll
