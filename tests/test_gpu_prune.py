@@ -172,3 +172,25 @@ def test_direct_run_equals_extended_run(cuda, monkeypatch, r, vn, degs, seed):
     monkeypatch.setattr(executor, "DIRECT", True)
     got = run(m)
     assert got.coeffs == want.coeffs and got.shape == want.shape
+
+
+def test_kernel_timing_hook(cuda):
+    """pdb_kernel_timing brackets every det_gj launch with events on its stream
+    (bench.py's roofline): one record per launch, positive device time."""
+    m = _dense(10, 2, (4, 4), 2)
+    pl = plan(m)
+    st = executor.PrimeStages(m, pl, staged=False)
+    st.forward(0)
+    native.kernel_timing(True)
+    try:
+        st.det_kernels(0)
+        st.det_kernels(0)
+        ms, launches = native.kernel_timing_read()
+    finally:
+        native.kernel_timing(False)
+    per_call = -(-st.dp.sel // st.chunk)
+    assert launches == 2 * per_call
+    assert ms > 0
+    native.kernel_timing(True)
+    assert native.kernel_timing_read() == (0.0, 0)
+    native.kernel_timing(False)
