@@ -268,79 +268,59 @@ static void format_range(const FmtCtx& cx, size_t lo, size_t hi, std::string& ou
 
 }  // namespace
 
-static PyObject* format_terms(PyObject*, PyObject* args) {
-  PyObject *terms, *variables;
-  int threads = 1;
-  if (!PyArg_ParseTuple(args, "O!O!i", &PyDict_Type, &terms, &PyTuple_Type, &variables, &threads)) return nullptr;
+// One coefficient into the term list (GIL held): its sign, |c| == 1, and for
+// huge or portable-build magnitudes the decimal digits made now.
+static bool fmt_add(std::vector<FmtTerm>& T, std::deque<std::string>& decs, PyObject* val) {
+#ifdef PDB_DIRECT_LONG
+  const uintptr_t tag = reinterpret_cast<const PyLongObject*>(val)->long_value.lv_tag;
+  const bool neg = (tag & 3) == 2;
+  const bool one = (tag >> _PyLong_NON_SIZE_BITS) == 1 && reinterpret_cast<const PyLongObject*>(val)->long_value.ob_digit[0] == 1;
+  const bool huge = (tag >> _PyLong_NON_SIZE_BITS) > 80;
+#else
+  PyObject* zero_obj = PyLong_FromLong(0);
+  const int n0 = PyObject_RichCompareBool(val, zero_obj, Py_LT);
+  Py_DECREF(zero_obj);
+  if (n0 < 0) return false;
+  const bool neg = n0 == 1;
+  PyObject* a1 = PyNumber_Absolute(val);
+  if (!a1) return false;
+  PyObject* one_obj = PyLong_FromLong(1);
+  const bool one = PyObject_RichCompareBool(a1, one_obj, Py_EQ) == 1;
+  Py_DECREF(one_obj);
+  Py_DECREF(a1);
+  const bool huge = true;   // portable build: every magnitude through the public API
+#endif
+  const std::string* dec = nullptr;
+  if (huge) {
+    PyObject* a = PyNumber_Absolute(val);
+    PyObject* str = a ? PyObject_Str(a) : nullptr;
+    Py_XDECREF(a);
+    if (!str) return false;
+    Py_ssize_t sn = 0;
+    const char* u = PyUnicode_AsUTF8AndSize(str, &sn);
+    decs.emplace_back(u, (size_t)sn);
+    Py_DECREF(str);
+    dec = &decs.back();
+  }
+  T.push_back(FmtTerm{nullptr, 0, val, neg, one, dec});
+  return true;
+}
+
+static bool fmt_names(PyObject* variables, std::vector<std::string>& names) {
   const int k = (int)PyTuple_GET_SIZE(variables);
-  std::vector<std::string> names((size_t)k);
+  names.assign((size_t)k, std::string());
   for (int a = 0; a < k; ++a) {
     Py_ssize_t n = 0;
     const char* u = PyUnicode_AsUTF8AndSize(PyTuple_GET_ITEM(variables, a), &n);
-    if (!u) return nullptr;
+    if (!u) return false;
     names[(size_t)a].assign(u, (size_t)n);
   }
-  const Py_ssize_t count = PyDict_GET_SIZE(terms);
-  std::vector<int64_t> exps;
-  exps.reserve((size_t)count * (size_t)(k > 0 ? k : 1));
-  std::vector<FmtTerm> T;
-  T.reserve((size_t)count);
-  Py_ssize_t pos = 0;
-  PyObject *key, *val;
-  // first pass: exponents (the vector must not reallocate once pointers are taken)
-  std::deque<std::string> decs;   // stable addresses
-  PyObject* zero_obj = PyLong_FromLong(0);
-  PyObject* one_obj = PyLong_FromLong(1);
-  PyObject* mone_obj = PyLong_FromLong(-1);
-  struct Drop { PyObject *a, *b, *c; ~Drop() { Py_XDECREF(a); Py_XDECREF(b); Py_XDECREF(c); } } drop{zero_obj, one_obj, mone_obj};
-  while (PyDict_Next(terms, &pos, &key, &val)) {
-    if (!PyTuple_CheckExact(key) || PyTuple_GET_SIZE(key) != k || !PyLong_CheckExact(val)) {
-      PyErr_SetString(PyExc_TypeError, "format_terms: keys must be k-tuples of ints and values ints");
-      return nullptr;
-    }
-    for (int a = 0; a < k; ++a) {
-      PyObject* x = PyTuple_GET_ITEM(key, a);
-      if (!PyLong_CheckExact(x)) {
-        PyErr_SetString(PyExc_TypeError, "format_terms: exponents must be ints");
-        return nullptr;
-      }
-      const long long e = PyLong_AsLongLong(x);
-      if (e == -1 && PyErr_Occurred()) return nullptr;
-      exps.push_back((int64_t)e);
-    }
-    if (k == 0) exps.push_back(0);
-    const int zero = PyObject_Not(val);
-    if (zero < 0) return nullptr;
-    if (zero) { exps.resize(exps.size() - (size_t)(k > 0 ? k : 1)); continue; }
-#ifdef PDB_DIRECT_LONG
-    const uintptr_t tag = reinterpret_cast<const PyLongObject*>(val)->long_value.lv_tag;
-    const int neg = (tag & 3) == 2;
-    const int one = (tag >> _PyLong_NON_SIZE_BITS) == 1 && reinterpret_cast<const PyLongObject*>(val)->long_value.ob_digit[0] == 1;
-#else
-    const int neg = PyObject_RichCompareBool(val, zero_obj, Py_LT);
-    const int one = PyObject_RichCompareBool(val, one_obj, Py_EQ) == 1 ||
-                    PyObject_RichCompareBool(val, mone_obj, Py_EQ) == 1;
-    if (neg < 0) return nullptr;
-#endif
-    const std::string* dec = nullptr;
-#ifdef PDB_DIRECT_LONG
-    const bool huge = (reinterpret_cast<const PyLongObject*>(val)->long_value.lv_tag >> _PyLong_NON_SIZE_BITS) > 80;
-#else
-    const bool huge = true;   // portable build: every magnitude through the public API
-#endif
-    if (huge) {
-      PyObject* a = PyNumber_Absolute(val);
-      PyObject* str = a ? PyObject_Str(a) : nullptr;
-      Py_XDECREF(a);
-      if (!str) return nullptr;
-      Py_ssize_t sn = 0;
-      const char* u = PyUnicode_AsUTF8AndSize(str, &sn);
-      decs.emplace_back(u, (size_t)sn);
-      Py_DECREF(str);
-      dec = &decs.back();
-    }
-    T.push_back(FmtTerm{nullptr, 0, val, neg == 1, one != 0, dec});
-  }
+  return true;
+}
+
+// Sort (graded lexicographic, highest first) and print the collected terms.
+static PyObject* fmt_finish(std::vector<FmtTerm>& T, std::vector<int64_t>& exps, int k,
+                            const std::vector<std::string>& names, int threads) {
   const size_t stride = (size_t)(k > 0 ? k : 1);
   for (size_t i = 0; i < T.size(); ++i) {
     T[i].e = exps.data() + i * stride;
@@ -349,7 +329,6 @@ static PyObject* format_terms(PyObject*, PyObject* args) {
     T[i].deg = d;
   }
   if (T.empty()) return PyUnicode_FromString("0");
-  // graded lexicographic, highest first: key (deg, e_0, ..., e_{k-1}) descending
   auto later = [k](const FmtTerm& x, const FmtTerm& y) {
     if (x.deg != y.deg) return x.deg > y.deg;
     for (int a = 0; a < k; ++a)
@@ -379,11 +358,10 @@ static PyObject* format_terms(PyObject*, PyObject* args) {
   }
   Py_END_ALLOW_THREADS
   const int nt = T.size() < 20000 ? 1 : nthreads;
-
   FmtCtx cx{&T, k, &names};
   std::vector<std::string> parts((size_t)nt);
-  // the coefficient objects are immutable and kept alive by the dict for the
-  // whole call: worker threads read their digits without the GIL
+  // the coefficient objects are immutable and kept alive by the caller's
+  // container for the whole call: worker threads read their digits without the GIL
   Py_BEGIN_ALLOW_THREADS
   std::vector<std::thread> pool;
   for (int j = 0; j < nt; ++j) {
@@ -414,6 +392,99 @@ static PyObject* format_terms(PyObject*, PyObject* args) {
   all.reserve(total);
   for (auto& s : parts) { all.append(s); std::string().swap(s); }
   return PyUnicode_DecodeUTF8(all.data(), (Py_ssize_t)all.size(), "strict");
+}
+
+static PyObject* format_terms(PyObject*, PyObject* args) {
+  PyObject *terms, *variables;
+  int threads = 1;
+  if (!PyArg_ParseTuple(args, "O!O!i", &PyDict_Type, &terms, &PyTuple_Type, &variables, &threads)) return nullptr;
+  std::vector<std::string> names;
+  if (!fmt_names(variables, names)) return nullptr;
+  const int k = (int)names.size();
+  const Py_ssize_t count = PyDict_GET_SIZE(terms);
+  std::vector<int64_t> exps;
+  exps.reserve((size_t)count * (size_t)(k > 0 ? k : 1));
+  std::vector<FmtTerm> T;
+  T.reserve((size_t)count);
+  std::deque<std::string> decs;   // stable addresses
+  Py_ssize_t pos = 0;
+  PyObject *key, *val;
+  while (PyDict_Next(terms, &pos, &key, &val)) {
+    if (!PyTuple_CheckExact(key) || PyTuple_GET_SIZE(key) != k || !PyLong_CheckExact(val)) {
+      PyErr_SetString(PyExc_TypeError, "format_terms: keys must be k-tuples of ints and values ints");
+      return nullptr;
+    }
+    const int zero = PyObject_Not(val);
+    if (zero < 0) return nullptr;
+    if (zero) continue;
+    for (int a = 0; a < k; ++a) {
+      PyObject* x = PyTuple_GET_ITEM(key, a);
+      if (!PyLong_CheckExact(x)) {
+        PyErr_SetString(PyExc_TypeError, "format_terms: exponents must be ints");
+        return nullptr;
+      }
+      const long long e = PyLong_AsLongLong(x);
+      if (e == -1 && PyErr_Occurred()) return nullptr;
+      exps.push_back((int64_t)e);
+    }
+    if (k == 0) exps.push_back(0);
+    if (!fmt_add(T, decs, val)) return nullptr;
+  }
+  return fmt_finish(T, exps, k, names, threads);
+}
+
+// format_dense(coeffs: tuple of ints (row-major over shape), shape: tuple, variables, threads) -> str:
+// the same text for a dense coefficient tensor (CoeffTensor) without building its terms() dict.
+static PyObject* format_dense(PyObject*, PyObject* args) {
+  PyObject *coeffs, *shape, *variables;
+  int threads = 1;
+  if (!PyArg_ParseTuple(args, "O!O!O!i", &PyTuple_Type, &coeffs, &PyTuple_Type, &shape, &PyTuple_Type, &variables,
+                        &threads))
+    return nullptr;
+  std::vector<std::string> names;
+  if (!fmt_names(variables, names)) return nullptr;
+  const int k = (int)names.size();
+  if (PyTuple_GET_SIZE(shape) != k) {
+    PyErr_SetString(PyExc_ValueError, "format_dense: shape and variables differ in length");
+    return nullptr;
+  }
+  std::vector<int64_t> dims((size_t)k);
+  Py_ssize_t n = 1;
+  for (int a = 0; a < k; ++a) {
+    dims[(size_t)a] = PyLong_AsLongLong(PyTuple_GET_ITEM(shape, a));
+    if (dims[(size_t)a] < 1) {
+      if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "format_dense: bad shape");
+      return nullptr;
+    }
+    n *= (Py_ssize_t)dims[(size_t)a];
+  }
+  if (PyTuple_GET_SIZE(coeffs) != n) {
+    PyErr_SetString(PyExc_ValueError, "format_dense: coefficient count does not fill the shape");
+    return nullptr;
+  }
+  std::vector<int64_t> exps;
+  std::vector<FmtTerm> T;
+  std::deque<std::string> decs;
+  std::vector<int64_t> idx((size_t)(k > 0 ? k : 1), 0);
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    PyObject* val = PyTuple_GET_ITEM(coeffs, i);
+    if (!PyLong_CheckExact(val)) {
+      PyErr_SetString(PyExc_TypeError, "format_dense: coefficients must be ints");
+      return nullptr;
+    }
+    const int zero = PyObject_Not(val);
+    if (zero < 0) return nullptr;
+    if (!zero) {
+      for (int a = 0; a < k; ++a) exps.push_back(idx[(size_t)a]);
+      if (k == 0) exps.push_back(0);
+      if (!fmt_add(T, decs, val)) return nullptr;
+    }
+    for (int a = k - 1; a >= 0; --a) {   // row-major successor of the multi-index
+      if (++idx[(size_t)a] < dims[(size_t)a]) break;
+      idx[(size_t)a] = 0;
+    }
+  }
+  return fmt_finish(T, exps, k, names, threads);
 }
 
 // ints_from_digits(digits: [count][D] u32 30-bit digits, ndig: uint8[count], index: int64[count] (ascending),
@@ -505,6 +576,8 @@ static PyMethodDef methods[] = {
     {"direct_path", direct_path, METH_NOARGS, "True if this build writes PyLong digits directly"},
     {"ints_from_digits", ints_from_digits, METH_VARARGS,
      "ints_from_digits(digits, ndig, index, neg, n, D) -> tuple of n ints from device-made 30-bit digit rows"},
+    {"format_dense", format_dense, METH_VARARGS,
+     "format_dense(coeffs, shape, variables, threads) -> format_terms of a dense coefficient tensor"},
     {"format_terms", format_terms, METH_VARARGS,
      "format_terms(terms, variables, threads) -> the reference's canonical polynomial text (parsing.py:211-225)"},
     {nullptr, nullptr, 0, nullptr}};

@@ -27,6 +27,12 @@ def format_polynomial(terms, variables) -> str:
     """Canonical text: graded lexicographic order, highest terms first."""
     variables = tuple(str(v) for v in variables)
     host = native.host_module()
+    if isinstance(terms, CoeffTensor) and len(terms.shape) == len(variables):
+        # straight from the dense coefficients: no terms() dict of 10^6-10^7 tuples
+        try:
+            return host.format_dense(terms.coeffs, tuple(int(n) for n in terms.shape), variables, _threads())
+        except TypeError:
+            pass
     if isinstance(terms, CoeffTensor):
         terms = terms.terms()
     if isinstance(terms, dict) and type(terms) is dict:

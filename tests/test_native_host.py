@@ -69,6 +69,11 @@ def test_formatter_portable_build_agrees(tmp_path):
     want = O.format_polynomial(terms, ("x", "y"))
     assert portable.format_terms(terms, ("x", "y"), 4) == want
     assert native.host_module().format_terms(terms, ("x", "y"), 4) == want
+    dense = [0] * 36
+    for (a, b), c in terms.items():
+        dense[a * 6 + b] = c
+    for mod in (portable, native.host_module()):
+        assert mod.format_dense(tuple(dense), (6, 6), ("x", "y"), 4) == want
 
 
 def test_ints_from_digits_matches_limb_path():
