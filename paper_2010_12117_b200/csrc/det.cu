@@ -371,17 +371,17 @@ static void launch_robust(PrimeCtx* ctx, Src src, const int32_t* ids, int r, con
   count_launch();
 }
 
-template <class Src, bool DFT8, int LPM, bool P31, int RPC>
+template <class Src, bool DFT8, int LPM, bool P31, int RPC, bool PAIR = false>
 static int launch_gj_geom(PrimeCtx* ctx, const GjGeom& g, Src src, const int32_t* ids, int64_t node_lo,
                           int64_t nodes, uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn,
                           cudaStream_t st) {
   const size_t smem = gj_smem(g);
-  if (cudaFuncSetAttribute(det_gj_kernel<Src, DFT8, LPM, P31, RPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(det_gj_kernel<Src, DFT8, LPM, P31, RPC, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return check_launch("det_gj attribute");
   int ctas_per_sm = 0;
   const int threads = g.M * LPM;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, det_gj_kernel<Src, DFT8, LPM, P31, RPC>, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, det_gj_kernel<Src, DFT8, LPM, P31, RPC, PAIR>, threads, smem);
   if (ctas_per_sm < 1) ctas_per_sm = 1;
   static const char* cenv = getenv("PDB_GJ_CTAS");   // experiments: cap resident CTAs per SM
   if (cenv && *cenv && atoi(cenv) > 0 && atoi(cenv) < ctas_per_sm) ctas_per_sm = atoi(cenv);
@@ -390,7 +390,7 @@ static int launch_gj_geom(PrimeCtx* ctx, const GjGeom& g, Src src, const int32_t
   const int grid = (int)(iters < cap ? iters : cap);
   if (grid < 1) return 0;
   const int kt = ktimer_start(st);
-  det_gj_kernel<Src, DFT8, LPM, P31, RPC><<<grid, threads, smem, st>>>(src, ids, node_lo, nodes, out, den, fc, fn, g, ctx->m);
+  det_gj_kernel<Src, DFT8, LPM, P31, RPC, PAIR><<<grid, threads, smem, st>>>(src, ids, node_lo, nodes, out, den, fc, fn, g, ctx->m);
   ktimer_stop(kt, st);
   count_launch();
   if (int rc = check_launch("det_gj")) return rc;
@@ -410,6 +410,21 @@ static int gj_lanes(int r) {
   return (RP == 48 || RP >= 72) ? 32 : PDB_GJ_LANES;
 }
 
+// Paired pivot blocks (det_gj_kernel<..., PAIR>) accumulate 17 products of
+// canonical residues: 17 (p-1)^2 < 2^64, and after hi(acc) -= 2p when hi >= 2p,
+// hi + p < 2^32 (REDC's bound).  p < 1.0417e9: every prime the reference plans from
+// its default prime_start = 10**9 for up to thousands of primes.
+static bool gj_pair_ok(uint32_t p) {
+  if (getenv("PDB_GJ_NO_PAIR")) return false;
+  const unsigned __int128 pm = p - 1;
+  const unsigned __int128 acc = 17 * pm * pm;
+  if (acc >> 64) return false;
+  const uint64_t hi = (uint64_t)(acc >> 32);
+  const uint64_t hi2 = hi >= 2ull * p ? hi - 2ull * p : hi;
+  const uint64_t hmax = hi2 > 2ull * p - 1 ? hi2 : 2ull * p - 1;
+  return hmax + p < (1ull << 32);
+}
+
 template <class Src, bool DFT8>
 static int launch_gj_mode(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int64_t node_lo, int64_t nodes,
                          uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
@@ -425,6 +440,9 @@ static int launch_gj_mode(PrimeCtx* ctx, int r, Src src, const int32_t* ids, int
   // 256-thread CTAs, the staged ones take any CTA size
   const bool rpc = (!DFT8 || g.M * PDB_GJ_LANES == 256) && !getenv("PDB_GJ_NO_RPC");
   if (ctx->m.fast()) {
+    if (g.RP == 40 && rpc && gj_pair_ok(ctx->m.p))
+      return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 40, true>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn,
+                                                                      st);
     if (g.RP == 40 && rpc)
       return launch_gj_geom<Src, DFT8, PDB_GJ_LANES, false, 40>(ctx, g, src, ids, node_lo, nodes, out, den, fc, fn, st);
     if (g.RP == 16 && rpc)

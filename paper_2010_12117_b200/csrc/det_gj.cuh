@@ -424,61 +424,149 @@ __device__ __forceinline__ void gj_st_sw(uint32_t* a, int sw, const uint32_t (&v
   }
 }
 
+// REDC of a <= 17-product accumulator (paired pivot blocks), canonical.  Valid
+// for p < PDB_PAIR_PMAX (gj_pair_ok): 17 (p-1)^2 < 2^64, and subtracting 2p from
+// hi(acc) (acc - 2p 2^32 == acc mod p) brings hi below 2^32 - p as REDC needs.
+__device__ __forceinline__ uint32_t gj_red17(uint64_t acc, const Mod32& m) {
+  const uint32_t lo = (uint32_t)acc;
+  const uint32_t hi = csub((uint32_t)(acc >> 32), 2u * m.p);
+  const uint32_t v = hi + m.p - umulhi32(lo * m.qinv, m.p);
+  return csub(csub(v, 2u * m.p), m.p);
+}
+
+// One TR x TC tile of the trailing update A[i0.., cc..] <- c*A + A[i0.., K..K+B-1] * negM[K..K+B-1][cc..].
 // P31: 2^30 <= p < 2^31 -- at most two products per reduction (2 p^2 < 2^63 keeps
-// hi(acc) + p < 2^32); the partial results are summed mod p.
-template <int TR, int TC, int LPM, bool P31, int B = GJ_B>
+// hi(acc) + p < 2^32); the partial results are summed mod p.  W17: B = 16 products
+// (two pivot blocks) + the scale in one accumulator, reduced by gj_red17.
+template <int TR, int TC, bool P31, int B, bool W17 = false>
+__device__ __forceinline__ void gj_ttile(uint32_t* A, int S, int K, int i0, int cc, int sw, uint32_t cR,
+                                         const Mod32& m) {
+  const uint32_t* npr = A + K * S;    // negM rows K..K+B-1
+  uint32_t a21[TR][B];
+  uint64_t acc[TR][TC];
+#pragma unroll
+  for (int a = 0; a < TR; ++a) {
+    const uint32_t* row = A + (i0 + a) * S;
+    gj_ld<B>(row + K, a21[a]);
+    uint32_t v[TC];
+    gj_ld_sw<TC>(row + cc, sw, v);
+#pragma unroll
+    for (int b = 0; b < TC; ++b) acc[a][b] = mad_wide(v[b], cR, 0ull);
+  }
+  uint32_t sum[TR][TC];
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    uint32_t nm[TC];
+    gj_ld_sw<TC>(npr + q * S + cc, sw, nm);
+#pragma unroll
+    for (int a = 0; a < TR; ++a)
+#pragma unroll
+      for (int b = 0; b < TC; ++b) {
+        const bool fresh = P31 && (q & 1);                   // q = 1, 3, 5, 7 open a new pair
+        acc[a][b] = mad_wide(a21[a][q], nm[b], fresh ? 0ull : acc[a][b]);
+        if (P31 && (q % 2 == 0 || q == B - 1)) {         // fold after q = 0, 2, 4, ..., B-1
+          const uint32_t v = gj_red2(acc[a][b], m);
+          sum[a][b] = q == 0 ? v : add_mod(sum[a][b], v, m.p);
+        }
+      }
+  }
+#pragma unroll
+  for (int a = 0; a < TR; ++a) {
+    uint32_t v[TC];
+#pragma unroll
+    for (int b = 0; b < TC; ++b) v[b] = P31 ? sum[a][b] : (W17 ? gj_red17(acc[a][b], m) : gj_red(acc[a][b], m));
+    gj_st_sw<TC>(A + (i0 + a) * S + cc, sw, v);
+  }
+}
+
+template <int TR, int TC, int LPM, bool P31, int B = GJ_B, bool W17 = false>
 __device__ __forceinline__ void gj_tpass(uint32_t* A, int S, int K, int mrem, uint32_t cR, int l, const Mod32& m) {
   const int c0 = K + B;
   const int ntc = mrem / TC;
   const int tiles = (mrem / TR) * ntc;
-  const uint32_t* npr = A + K * S;    // negM rows K..K+7
   int ti = l / ntc, tc = l - (l / ntc) * ntc;
   const int dti = LPM / ntc, dtc = LPM - (LPM / ntc) * ntc;
   PDB_UNROLL(PDB_GJ_TUNROLL)
   for (int w = l; w < tiles; w += LPM) {
-    const int i0 = c0 + TR * ti, cc = c0 + TC * tc;
     // 8-wide tiles: odd tile rows visit their two 16-byte chunks in swapped order,
     // so the 8 lanes of a quarter-warp (two tile rows x four column tiles) hit 8
     // distinct bank groups; column v of this lane's tile is physical column
     // cc + ((v + sw) mod 8).
     const int sw = (TC == 8 && (ti & 1)) ? 4 : 0;
-    uint32_t a21[TR][B];
-    uint64_t acc[TR][TC];
-#pragma unroll
-    for (int a = 0; a < TR; ++a) {
-      const uint32_t* row = A + (i0 + a) * S;
-      gj_ld<B>(row + K, a21[a]);
-      uint32_t v[TC];
-      gj_ld_sw<TC>(row + cc, sw, v);
-#pragma unroll
-      for (int b = 0; b < TC; ++b) acc[a][b] = mad_wide(v[b], cR, 0ull);
-    }
-    uint32_t sum[TR][TC];
-#pragma unroll
-    for (int q = 0; q < B; ++q) {
-      uint32_t nm[TC];
-      gj_ld_sw<TC>(npr + q * S + cc, sw, nm);
-#pragma unroll
-      for (int a = 0; a < TR; ++a)
-#pragma unroll
-        for (int b = 0; b < TC; ++b) {
-          const bool fresh = P31 && (q & 1);                   // q = 1, 3, 5, 7 open a new pair
-          acc[a][b] = mad_wide(a21[a][q], nm[b], fresh ? 0ull : acc[a][b]);
-          if (P31 && (q % 2 == 0 || q == B - 1)) {         // fold after q = 0, 2, 4, ..., B-1
-            const uint32_t v = gj_red2(acc[a][b], m);
-            sum[a][b] = q == 0 ? v : add_mod(sum[a][b], v, m.p);
-          }
-        }
-    }
-#pragma unroll
-    for (int a = 0; a < TR; ++a) {
-      uint32_t v[TC];
-#pragma unroll
-      for (int b = 0; b < TC; ++b) v[b] = P31 ? sum[a][b] : gj_red(acc[a][b], m);
-      gj_st_sw<TC>(A + (i0 + a) * S + cc, sw, v);
-    }
+    gj_ttile<TR, TC, P31, B, W17>(A, S, K, c0 + TR * ti, c0 + TC * tc, sw, cR, m);
     ti += dti; tc += dtc;
     if (tc >= ntc) { tc -= ntc; ++ti; }
+  }
+}
+
+// Trailing update of a 24 x 24 region at (c0, c0) with 16 lanes and no idle
+// lane: 64 2x4 tiles (4 passes: rows c0..c0+23 x columns c0..c0+19, and rows
+// c0+16..c0+23 x columns c0+20..c0+23) and 16 1x4 tiles (one pass: rows
+// c0..c0+15 x columns c0+20..c0+23), instead of 72 2x4 tiles in 4.5 passes.
+template <bool P31, int B, bool W17 = false>
+__device__ __forceinline__ void gj_tpass24(uint32_t* A, int S, int K, int c0, uint32_t cR, int l, const Mod32& m) {
+  PDB_UNROLL(PDB_GJ_TUNROLL)
+  for (int w = l; w < 64; w += 16) {
+    const bool main = w < 60;
+    const int i0 = c0 + (main ? 2 * (w / 5) : 16 + 2 * (w - 60));
+    const int cc = c0 + (main ? 4 * (w % 5) : 20);
+    gj_ttile<2, 4, P31, B, W17>(A, S, K, i0, cc, 0, cR, m);
+  }
+  gj_ttile<1, 4, P31, B, W17>(A, S, K, c0 + l, c0 + 20, 0, cR, m);
+}
+
+// First block of a pivot pair: the trailing update of block K restricted to the
+// panel the next block reads -- its pivot rows K+8..K+15 (all trailing columns)
+// and the column strip K+8..K+15 of the rows below.  The rest of the trailing
+// matrix is updated once for both blocks (gj_tpass<..., 16, true>).
+// Panel of block K with 32 trailing columns and 16 lanes, no idle lane: 48 2x4
+// tiles (rows c0..c0+7 x 32 columns, rows c0+8..c0+23 x columns c0..c0+7) in 3
+// passes and 16 1x4 tiles (rows c0+24..c0+31 x columns c0..c0+7) in one.
+__device__ __forceinline__ void gj_tpass_panel32(uint32_t* A, int S, int K, uint32_t cR, int l, const Mod32& m) {
+  const int c0 = K + GJ_B;
+  for (int w = l; w < 48; w += 16) {
+    const bool top = w < 32;
+    const int i0 = c0 + (top ? 2 * (w >> 3) : GJ_B + 2 * ((w - 32) >> 1));
+    const int cc = c0 + (top ? 4 * (w & 7) : 4 * (w & 1));
+    gj_ttile<2, 4, false, GJ_B>(A, S, K, i0, cc, 0, cR, m);
+  }
+  gj_ttile<1, 4, false, GJ_B>(A, S, K, c0 + 24 + (l >> 1), c0 + 4 * (l & 1), 0, cR, m);
+}
+
+template <int TR, int TC, int LPM>
+__device__ __forceinline__ void gj_tpass_panel(uint32_t* A, int S, int K, int mrem, uint32_t cR, int l,
+                                               const Mod32& m) {
+  const int c0 = K + GJ_B;
+  const int n1c = mrem / TC;
+  const int t1 = (GJ_B / TR) * n1c;                          // rows c0..c0+7, every trailing column
+  constexpr int n2c = GJ_B / TC;
+  const int t2 = ((mrem - GJ_B) / TR) * n2c;                 // rows c0+8.., columns c0..c0+7
+  for (int w = l; w < t1 + t2; w += LPM) {
+    int i0, cc;
+    if (w < t1) {
+      i0 = c0 + TR * (w / n1c);
+      cc = c0 + TC * (w % n1c);
+    } else {
+      const int w2 = w - t1;
+      i0 = c0 + GJ_B + TR * (w2 / n2c);
+      cc = c0 + TC * (w2 % n2c);
+    }
+    gj_ttile<TR, TC, false, GJ_B>(A, S, K, i0, cc, 0, cR, m);
+  }
+}
+
+// negM rows K..K+7, columns c0.. (RP - c0 words each, a multiple of 4) scaled by cR (Montgomery form)
+template <int LPM>
+__device__ __forceinline__ void gj_scale_rows(uint32_t* A, int S, int K, int c0, int ncols, uint32_t cR, int l,
+                                              const Mod32& m) {
+  const int per_row = ncols / 4;
+  for (int w = l; w < GJ_B * per_row; w += LPM) {
+    uint32_t* a = A + (K + w / per_row) * S + c0 + 4 * (w % per_row);
+    uint32_t v[4];
+    gj_ld<4>(a, v);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) v[b] = gj_mont(v[b], cR, m);
+    gj_st<4>(a, v);
   }
 }
 
@@ -511,6 +599,39 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
 // block of A12 and RPI rows of negX (16 B loads) for RPI*TC*8 MACs.  Items are
 // numbered column-group major, so the lanes sharing a column group work in the
 // same pass; they read it completely before any of them overwrites it.
+// One M-pass item: rows rg*RPI.. of negM, columns c..c+TC-1 (reads negX and the
+// 8 x TC block of A12 at column c; the caller stores after a __syncwarp).
+template <int RPI, int TC, bool P31, int B>
+__device__ __forceinline__ void gj_mitem(const uint32_t* A, const uint32_t* NX, int S, int K, int c, int rg,
+                                         uint32_t (&res)[RPI][TC], const Mod32& m) {
+  uint32_t x[RPI][B];   // this item's negX rows, 16 B loads
+#pragma unroll
+  for (int t = 0; t < RPI; ++t) gj_ld<B>(NX + gj_nx_row(rg * RPI + t), x[t]);
+  uint64_t acc[RPI][TC];
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    uint32_t a[TC];
+    gj_ld<TC>(A + (K + q) * S + c, a);
+#pragma unroll
+    for (int t = 0; t < RPI; ++t)
+#pragma unroll
+      for (int b = 0; b < TC; ++b) {
+        const bool fresh = q == 0 || (P31 && q % 2 == 0);
+        acc[t][b] = mad_wide(x[t][q], a[b], fresh ? 0ull : acc[t][b]);
+        if (P31 && (q & 1)) {                              // fold pairs (0,1), (2,3), ...
+          const uint32_t v = gj_red2(acc[t][b], m);
+          res[t][b] = q == 1 ? v : add_mod(res[t][b], v, m.p);
+        }
+      }
+  }
+  if (!P31) {
+#pragma unroll
+    for (int t = 0; t < RPI; ++t)
+#pragma unroll
+      for (int b = 0; b < TC; ++b) res[t][b] = gj_red(acc[t][b], m);
+  }
+}
+
 template <int RPI, int TC, int LPM, bool P31, int B = GJ_B>
 __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S, int K, int mrem, int l,
                                          unsigned omask, const Mod32& m) {
@@ -523,39 +644,35 @@ __device__ __forceinline__ void gj_mpass(uint32_t* A, const uint32_t* NX, int S,
     const int cg = w / NRG, rg = w - (w / NRG) * NRG;
     const int c = K + B + TC * cg;
     uint32_t res[RPI][TC];
-    if (act) {
-      uint32_t x[RPI][B];   // this item's negX rows, 16 B loads
-#pragma unroll
-      for (int t = 0; t < RPI; ++t) gj_ld<B>(NX + gj_nx_row(rg * RPI + t), x[t]);
-      uint64_t acc[RPI][TC];
-#pragma unroll
-      for (int q = 0; q < B; ++q) {
-        uint32_t a[TC];
-        gj_ld<TC>(A + (K + q) * S + c, a);
-#pragma unroll
-        for (int t = 0; t < RPI; ++t)
-#pragma unroll
-          for (int b = 0; b < TC; ++b) {
-            const bool fresh = q == 0 || (P31 && q % 2 == 0);
-            acc[t][b] = mad_wide(x[t][q], a[b], fresh ? 0ull : acc[t][b]);
-            if (P31 && (q & 1)) {                              // fold pairs (0,1), (2,3), ...
-              const uint32_t v = gj_red2(acc[t][b], m);
-              res[t][b] = q == 1 ? v : add_mod(res[t][b], v, m.p);
-            }
-          }
-      }
-      if (!P31) {
-#pragma unroll
-        for (int t = 0; t < RPI; ++t)
-#pragma unroll
-          for (int b = 0; b < TC; ++b) res[t][b] = gj_red(acc[t][b], m);
-      }
-    }
+    if (act) gj_mitem<RPI, TC, P31, B>(A, NX, S, K, c, rg, res, m);
     if (NRG > 1) __syncwarp(omask);
     if (act) {
 #pragma unroll
       for (int t = 0; t < RPI; ++t) gj_st<TC>(A + (K + rg * RPI + t) * S + c, res[t]);
     }
+  }
+}
+
+// M pass over 24 trailing columns with 16 lanes and no idle lane: one pass of
+// 2x4 items over columns 0..15, one of 1x4 items over columns 16..23 (2x4 items
+// alone need 1.5 passes, and a pass costs its full issue whatever the lanes do).
+template <bool P31, int B = GJ_B>
+__device__ __forceinline__ void gj_mpass24(uint32_t* A, const uint32_t* NX, int S, int K, int l, unsigned omask,
+                                           const Mod32& m) {
+  {
+    const int rg = l & 3, c = K + B + 4 * (l >> 2);
+    uint32_t res[2][4];
+    gj_mitem<2, 4, P31, B>(A, NX, S, K, c, rg, res, m);
+    __syncwarp(omask);
+    gj_st<4>(A + (K + 2 * rg) * S + c, res[0]);
+    gj_st<4>(A + (K + 2 * rg + 1) * S + c, res[1]);
+  }
+  {
+    const int rg = l & 7, c = K + B + 16 + 4 * (l >> 3);
+    uint32_t res[1][4];
+    gj_mitem<1, 4, P31, B>(A, NX, S, K, c, rg, res, m);
+    __syncwarp(omask);
+    gj_st<4>(A + (K + rg) * S + c, res[0]);
   }
 }
 
@@ -577,6 +694,17 @@ __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, in
   else gj_mpass<1, 2, LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
 }
 
+// f(integral_constant<int, K>) for K = FIRST, FIRST + STEP, ... < END: a loop whose
+// unrolling does not depend on the compiler's heuristics (the block loop of the
+// compile-time-order kernels must unroll so every shared-memory offset is an immediate)
+template <int K, int END, int STEP, class F>
+__device__ __forceinline__ void gj_unrolled(F&& f) {
+  if constexpr (K < END) {
+    f(std::integral_constant<int, K>{});
+    gj_unrolled<K + STEP, END, STEP>(f);
+  }
+}
+
 // ---- the kernel ------------------------------------------------------------------------------
 #ifndef PDB_GJ_GELAST
 #define PDB_GJ_GELAST 1   // last pivot block: elimination without the Gauss-Jordan back part
@@ -587,13 +715,16 @@ __device__ __forceinline__ void gj_mpass_any(uint32_t* A, const uint32_t* NX, in
 // RPC > 0: the padded order is the compile-time constant RPC (row stride
 // gj_row_stride(RPC)); the block loop unrolls, every pass sees a constant
 // trailing size, and all shared-memory addressing folds into immediates.
-template <class Src, bool DFT8, int LPM, bool P31, int RPC>
+// PAIR: the first two pivot blocks share one trailing update (17 products per
+// reduction, p < PDB_PAIR_PMAX; compile-time orders RPC >= 32 only).
+template <class Src, bool DFT8, int LPM, bool P31, int RPC, bool PAIR = false>
 __global__ void __launch_bounds__(256, PDB_GJ_MINB)
 det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t nodes,
               uint32_t* __restrict__ num_out, uint32_t* __restrict__ den_out,
               unsigned long long* __restrict__ flag_count, int64_t* __restrict__ flag_nodes, GjGeom g, Mod32 m) {
   static_assert(LPM == 8 || LPM == 16 || LPM == 32, "8, 16 or 32 lanes per matrix");
   static_assert(RPC % GJ_B == 0, "compile-time order must be padded to the block size");
+  static_assert(!PAIR || (RPC >= 32 && !P31), "paired blocks: compile-time order >= 32, p < 2^30");
   // Pivot-block schedule: blocks of 8, except that the staged compile-time
   // kernels (orders 40 and 16, p < 2^30, 16 lanes) eliminate their last 8
   // columns as two blocks of 4 (a 4x4 Gauss-Jordan costs a third of an 8x8 one
@@ -653,6 +784,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
     // C8 / C4: products of the running c-prefix Q taken before each block of 8 / 4
     // (det A picks up Q^B per block: den *= C8^8 C4^4 at the end)
     uint32_t num = one, den = one, Q = one, C8 = one, C4 = one;
+    uint32_t cPrev = one;   // c of the first block of a pair
 
     // One block of B pivots at column K; false if a pivot vanished.
     auto block = [&](auto Bc, int K) -> bool {
@@ -719,10 +851,34 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       for (int k = 0; k < EPL; ++k) NX[gj_nx_row(pj) + pc + k] = v[k] ? p - v[k] : 0u;
       __syncwarp(omask);
       // ---------------- M: negM = negX * A12, in place in the pivot rows ----------------
-      if (PDB_GJ_ABL != 1) gj_mpass_any<LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
+      // compile-time orders with 16 lanes: the idle-lane-free variants where mrem = 24
+      constexpr bool FIT = RPC > 0 && LPM == 16 && B == GJ_B;
+      if (PDB_GJ_ABL == 1) {
+      } else if (FIT && mrem == 24) {
+        gj_mpass24<P31, B>(A, NX, S, K, l, omask, m);
+      } else {
+        gj_mpass_any<LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
+      }
       __syncwarp(omask);
       // ---------------- T: trailing rows ----------------
-      if (PDB_GJ_ABL != 2) gj_tpass_any<LPM, P31, B>(A, S, K, mrem, cR, l, m);
+      if (PAIR && K == 0) {
+        // first block of the pair: only the panel the second block reads
+        cPrev = cR;
+        if (FIT && mrem == 32) gj_tpass_panel32(A, S, K, cR, l, m);
+        else gj_tpass_panel<2, 4, LPM>(A, S, K, mrem, cR, l, m);
+      } else if (PAIR && K == GJ_B) {
+        // second block: c1 * negM0 beside negM1, then one 16-deep update with scale c0 c1:
+        // c1 (c0 A33 + A31 negM0) + A32' negM1 (A32' = the panel strip of block 0)
+        gj_scale_rows<LPM>(A, S, 0, K + B, mrem, cR, l, m);
+        __syncwarp(omask);
+        if (FIT && mrem == 24) gj_tpass24<false, 2 * GJ_B, true>(A, S, 0, K + B, gj_mont(cPrev, cR, m), l, m);
+        else gj_tpass<2, 4, LPM, false, 2 * GJ_B, true>(A, S, 0, mrem, gj_mont(cPrev, cR, m), l, m);
+      } else if (PDB_GJ_ABL == 2) {
+      } else if (FIT && mrem == 24) {
+        gj_tpass24<P31, B>(A, S, K, K + B, cR, l, m);
+      } else {
+        gj_tpass_any<LPM, P31, B>(A, S, K, mrem, cR, l, m);
+      }
       __syncwarp(omask);
       return true;
     };
@@ -732,12 +888,10 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       // e.g. RPC = 40: 8 8 8 8 | 4 4 (TAIL4 = 8) -- every K and block size a constant
       constexpr int K8 = RPC - TAIL4;
       static_assert(K8 % GJ_B == 0 && TAIL4 % 4 == 0, "tail split");
-#pragma unroll
-      for (int K = 0; K < K8; K += 8)
-        if (ok && !block(std::integral_constant<int, 8>{}, K)) ok = false;
-#pragma unroll
-      for (int K = K8; K < RPC; K += 4)
-        if (ok && !block(std::integral_constant<int, 4>{}, K)) ok = false;
+      gj_unrolled<0, K8, 8>([&](auto Kc) { if (ok && !block(std::integral_constant<int, 8>{}, Kc())) ok = false; });
+      gj_unrolled<K8, RPC, 4>([&](auto Kc) { if (ok && !block(std::integral_constant<int, 4>{}, Kc())) ok = false; });
+    } else if constexpr (RPC > 0) {
+      gj_unrolled<0, RPC, GJ_B>([&](auto Kc) { if (ok && !block(std::integral_constant<int, GJ_B>{}, Kc())) ok = false; });
     } else {
 #pragma unroll
       for (int K = 0; K < RP; K += GJ_B)

@@ -493,6 +493,28 @@ def test_resume_reference_written_partial_workspace(cuda, tmp_path):
     assert again == []
 
 
+@pytest.mark.parametrize("p", [1000000513, 1041682561, 1041682661])
+@pytest.mark.parametrize("r", [33, 40])
+def test_paired_pivot_blocks_at_the_accumulator_bound(cuda, r, p, monkeypatch):
+    """Order-40 kernels update the trailing matrix of their first two pivot
+    blocks in one pass (17 products per reduction) when p < 1.0417e9:
+    1041682561 is the largest prime inside that bound (entries near p - 1 are
+    the worst case), 1041682661 the smallest outside it (unpaired kernel).  Both
+    equal the oracle and the unpaired kernel (PDB_GJ_NO_PAIR=1); the fused C5
+    kernel is paired too (test_c5_determinants_at_sampled_nodes)."""
+    spec = PrimeSpec(p, p - 1, 0, 1)
+    rng = np.random.default_rng(p % 977 + r)
+    mats = rng.integers(0, p, (400, r, r))
+    mats[::3] = p - 1 - rng.integers(0, 3, (len(mats[::3]), r, r))   # entries at the top of the range
+    mats[::11, 0, 0] = 0
+    mats[5::13, 9, :] = 0                                           # singular inside the second block
+    grids = [mats[:, e // r, e % r] for e in range(r * r)]
+    want = O.det_grid(grids, r, p).tolist()
+    assert det_grid(grids, r, spec).tolist() == want
+    monkeypatch.setenv("PDB_GJ_NO_PAIR", "1")
+    assert det_grid(grids, r, spec).tolist() == want
+
+
 @pytest.mark.parametrize("r", [13, 16, 21, 24, 30, 32, 36, 40])
 def test_compile_time_and_runtime_order_kernels_agree(cuda, r, monkeypatch):
     """Padded orders 16, 24, 32 and 40 run compile-time-order kernels (the staged
