@@ -599,6 +599,165 @@ __device__ __forceinline__ void gj_tpass_any(uint32_t* A, int S, int K, int mrem
 // block of A12 and RPI rows of negX (16 B loads) for RPI*TC*8 MACs.  Items are
 // numbered column-group major, so the lanes sharing a column group work in the
 // same pass; they read it completely before any of them overwrites it.
+// ---- P: division-free Gauss-Jordan on a B x B pivot block ----------------------------
+// Lane l holds EPL = B / (LPM / B) entries of row pj, columns pc..pc+EPL-1.  On
+// return v holds X with X * A11 = lam * I (lam = prod of the pivots z_s); zl is
+// lambda_pj (the pivot prefix product when row pj was the pivot row) and zlast
+// the last pivot, so det(A11) = zlast / (lambda_1 ... lambda_{B-2}).  lam == 0
+// iff a pivot vanished.  GE: only the pivots are needed (last block): dead
+// columns are skipped.
+struct GjPiv {
+  uint32_t lam, zl, zlast;
+};
+template <int B, int LPM, bool LAZY, int EPL>
+__device__ __forceinline__ GjPiv gj_gauss_jordan(uint32_t (&v)[EPL], int pj, int pc, int l, unsigned omask, bool ge,
+                                                 const Mod32& m) {
+  constexpr int LPR = LPM / B;
+  static_assert(EPL == B / LPR, "entries per lane");
+  const uint32_t p = m.p, one = m.r1;
+  auto lazy_canon = [&](uint32_t x) { return LAZY ? csub(x, p) : x; };
+  uint32_t lam = one, zl = one, zlast = one;
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    // LAZY: pivot-block entries stay in [0, 2p) between steps (only the shuffled
+    // pivot z and multiplier t are made canonical): with zz, nn <= p and a, b < 2p
+    // the two products sum below 4 p^2, so REDC returns < hi + p < 2p (p < 2^30)
+    const uint32_t z = lazy_canon(__shfl_sync(omask, v[s % EPL], s * LPR + s / EPL, LPM));
+    const uint32_t t = lazy_canon(__shfl_sync(omask, v[s % EPL], pj * LPR + s / EPL, LPM));
+    // last block (no trailing rows): only det(A11) is needed, i.e. the pivots --
+    // Gaussian elimination suffices, and column slots k whose column is <= s in
+    // every lane of the group (B - EPL + k <= s) are dead from step s on
+    auto live = [&](int k) { return !ge || B - EPL + k > s; };
+    uint32_t prow[EPL];
+#pragma unroll
+    for (int k = 0; k < EPL; ++k)
+      if (live(k)) prow[k] = __shfl_sync(omask, v[k], s * LPR + l % LPR, LPM);
+    // Other rows: z v - t prow, with -t lam at column s (the identity column of
+    // row s is lam there).  Row s is scaled by lam = prod_{t<s} z_t instead
+    // (lam * v; lam^2 at column s): then every row ends up scaled by c =
+    // prod z overall, so the in-place inverse part is X = c A11^-1 itself.
+    const bool piv = pj == s;
+    zl = piv ? lam : zl;
+    const uint32_t zz = piv ? lam : z;
+    const uint32_t nn = piv ? 0u : p - t;   // p - t in (0, p]: a valid 2-product multiplier
+#pragma unroll
+    for (int k = 0; k < EPL; ++k) {
+      if (!live(k)) continue;
+      uint32_t a = v[k], b = prow[k];
+      if (k == s % EPL) {   // the only element of this lane that can sit in column s
+        const bool diag = pc == s - s % EPL;
+        a = diag ? (piv ? lam : 0u) : a;
+        b = diag ? lam : b;
+      }
+      const uint64_t acc = mad_wide(zz, a, mad_wide(nn, b, 0ull));
+      v[k] = LAZY ? gj_redc(acc, m) : gj_red2(acc, m);
+    }
+    if (s == B - 1) zlast = z;
+    lam = gj_mont(lam, z, m);
+  }
+  return {lam, zl, zlast};
+}
+
+// ---- P by 4x4 blocks (8x8 pivot block, 16 lanes: one 4x4 entry per lane) --------------
+// A11 = [[A, B], [C, D]].  Gauss-Jordan on A (X_A = a A^-1), N = -X_A B,
+// S = a D + C N = a Sigma (Sigma = D - C A^-1 B), Gauss-Jordan on S
+// (X_S = s S^-1), then X = c A11^-1 with c = a s from the block inverse:
+//   Y = a X_S = s Sigma^-1,  X22 = a Y,  X12 = N Y,  Z = X_S (C X_A),
+//   X21 = -a Z,  X11 = s X_A - N Z.
+// Two 4-step eliminations (2 products and a reduction per entry and step) plus
+// six 4x4 products with one reduction per 4-5 products: ~720 products and ~270
+// reductions per block against 1024 and 512 for the 8-step elimination.
+// det(A11) = det(A) det(S) / a^4: the a^4 is collected in aprod (den *= aprod^4
+// once per node).  Scratch: X_A and N in negX rows 0-3, then the dead pivot
+// block itself.  Returns false if a pivot vanished (A or S singular, i.e. a
+// leading principal minor of A11 is zero -- the same nodes the 8-step
+// elimination flags).
+__device__ __forceinline__ bool gj_pinv44(uint32_t* A, uint32_t* NX, int S, int K, int l, unsigned omask,
+                                          const Mod32& m, uint32_t& num, uint32_t& den, uint32_t& aprod,
+                                          uint32_t& cR) {
+  const uint32_t p = m.p, one = m.r1;
+  const int i = l >> 2, j = l & 3;
+  uint32_t* P0 = A + K * S + K;   // the pivot block, row stride S
+  auto neg = [&](uint32_t x) { return x ? p - x : 0u; };
+  // X_A
+  uint32_t xa[1] = {P0[i * S + j]};
+  const GjPiv ga = gj_gauss_jordan<4, 16, false>(xa, i, j, l, omask, false, m);
+  if (ga.lam == 0) return false;
+  const uint32_t aR = ga.lam;
+  uint32_t crow[4];
+  gj_ld<4>(P0 + (4 + i) * S, crow);
+  const uint32_t dv = P0[(4 + i) * S + 4 + j];
+  NX[i * GJ_B + j] = xa[0];
+  __syncwarp(omask);
+  // N = -X_A B
+  {
+    uint32_t xr[4];
+    gj_ld<4>(NX + i * GJ_B, xr);
+    uint64_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc = mad_wide(xr[q], P0[q * S + 4 + j], acc);
+    NX[i * GJ_B + 4 + j] = neg(gj_red(acc, m));
+  }
+  __syncwarp(omask);
+  // S = a D + C N
+  uint32_t sv[1];
+  {
+    uint64_t acc = mad_wide(dv, aR, 0ull);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc = mad_wide(crow[q], NX[q * GJ_B + 4 + j], acc);
+    sv[0] = gj_red(acc, m);
+  }
+  const GjPiv gs = gj_gauss_jordan<4, 16, false>(sv, i, j, l, omask, false, m);
+  if (gs.lam == 0) return false;
+  const uint32_t sR = gs.lam, xs = sv[0];
+  const uint32_t y = gj_mont(xs, aR, m);   // Y = a X_S
+  __syncwarp(omask);                       // every read of the pivot block is done: scratch from here
+  P0[i * S + j] = xs;                      // X_S at the A position
+  P0[i * S + 4 + j] = y;                   // Y at the B position
+  {
+    uint64_t acc = 0;                      // P1 = C X_A at the C position
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc = mad_wide(crow[q], NX[q * GJ_B + j], acc);
+    P0[(4 + i) * S + j] = gj_red(acc, m);
+  }
+  __syncwarp(omask);
+  uint32_t zp;
+  {
+    uint32_t xr[4];                        // Z = X_S P1, -Z at the D position
+    gj_ld<4>(P0 + i * S, xr);
+    uint64_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc = mad_wide(xr[q], P0[(4 + q) * S + j], acc);
+    zp = gj_red(acc, m);
+  }
+  P0[(4 + i) * S + 4 + j] = neg(zp);
+  __syncwarp(omask);
+  uint32_t x11, x12;
+  {
+    uint32_t nr[4];                        // X12 = N Y, X11 = s X_A + N (-Z)
+    gj_ld<4>(NX + i * GJ_B + 4, nr);
+    uint64_t a12 = 0, a11 = mad_wide(xa[0], sR, 0ull);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      a12 = mad_wide(nr[q], P0[q * S + 4 + j], a12);
+      a11 = mad_wide(nr[q], P0[(4 + q) * S + 4 + j], a11);
+    }
+    x12 = gj_red(a12, m);
+    x11 = gj_red(a11, m);
+  }
+  __syncwarp(omask);
+  NX[gj_nx_row(i) + j] = neg(x11);
+  NX[gj_nx_row(i) + 4 + j] = neg(x12);
+  NX[gj_nx_row(4 + i) + j] = gj_mont(zp, aR, m);            // -X21 = a Z
+  NX[gj_nx_row(4 + i) + 4 + j] = gj_mont(y, neg(aR), m);    // -X22 = -a Y
+  // det(A) det(S): lambda_1, lambda_2 of A on lanes (1, 0), (2, 0), of S on (1, 1), (2, 1)
+  den = gj_mont(den, (i >= 1 && i <= 2 && j < 2) ? (j == 0 ? ga.zl : gs.zl) : one, m);
+  num = gj_mont(num, gj_mont(ga.zlast, gs.zlast, m), m);
+  aprod = gj_mont(aprod, aR, m);
+  cR = gj_mont(aR, sR, m);
+  return true;
+}
+
 // One M-pass item: rows rg*RPI.. of negM, columns c..c+TC-1 (reads negX and the
 // 8 x TC block of A12 at column c; the caller stores after a __syncwarp).
 template <int RPI, int TC, bool P31, int B>
@@ -706,6 +865,12 @@ __device__ __forceinline__ void gj_unrolled(F&& f) {
 }
 
 // ---- the kernel ------------------------------------------------------------------------------
+#ifndef PDB_GJ_P44
+#define PDB_GJ_P44 1   // 8x8 pivot blocks with trailing rows inverted by 4x4 blocks (gj_pinv44)
+#endif
+#ifndef PDB_GJ_LAZYP
+#define PDB_GJ_LAZYP 1   // pivot-block entries in [0, 2p) between Gauss-Jordan steps (p < 2^30)
+#endif
 #ifndef PDB_GJ_GELAST
 #define PDB_GJ_GELAST 1   // last pivot block: elimination without the Gauss-Jordan back part
 #endif
@@ -785,6 +950,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
     // (det A picks up Q^B per block: den *= C8^8 C4^4 at the end)
     uint32_t num = one, den = one, Q = one, C8 = one, C4 = one;
     uint32_t cPrev = one;   // c of the first block of a pair
+    uint32_t aprod = one;   // 4x4-block pivot blocks: product of the a's (den *= aprod^4)
 
     // One block of B pivots at column K; false if a pivot vanished.
     auto block = [&](auto Bc, int K) -> bool {
@@ -794,65 +960,40 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       static_assert(EPL >= 1, "block narrower than the lane group");
       const int pj = l / LPR, pc = EPL * (l % LPR);   // my pivot-block row / first column
       const int mrem = RP - K - B;
-      // ---------------- P: Gauss-Jordan on the pivot block ----------------
-      uint32_t v[EPL];
-      {
-        const uint32_t* src_row = A + (K + pj) * S + K + pc;
+      // compile-time orders with 16 lanes: the idle-lane-free variants where mrem = 24
+      constexpr bool FIT = RPC > 0 && LPM == 16 && B == GJ_B;
+      // ---------------- P: the pivot block -> X = c A11^-1 (negated into NX), c ----------------
+      uint32_t cR;
+      if (PDB_GJ_P44 && FIT && !P31 && mrem > 0) {
+        if (!gj_pinv44(A, NX, S, K, l, omask, m, num, den, aprod, cR)) return false;
+      } else {
+        uint32_t v[EPL];
+        {
+          const uint32_t* src_row = A + (K + pj) * S + K + pc;
 #pragma unroll
-        for (int k = 0; k < EPL; ++k) v[k] = src_row[k];
-      }
-      uint32_t lam = one, zl = one, zlast = one;
-#pragma unroll
-      for (int s = 0; s < B; ++s) {
-        const uint32_t z = __shfl_sync(omask, v[s % EPL], s * LPR + s / EPL, LPM);
-        const uint32_t t = __shfl_sync(omask, v[s % EPL], pj * LPR + s / EPL, LPM);
-        // last block (no trailing rows): only det(A11) is needed, i.e. the pivots --
-        // Gaussian elimination suffices, and column slots k whose column is <= s in
-        // every lane of the group (B - EPL + k <= s) are dead from step s on
-        auto live = [&](int k) { return !(PDB_GJ_GELAST && mrem == 0) || B - EPL + k > s; };
-        uint32_t prow[EPL];
-#pragma unroll
-        for (int k = 0; k < EPL; ++k)
-          if (live(k)) prow[k] = __shfl_sync(omask, v[k], s * LPR + l % LPR, LPM);
-        // Other rows: z v - t prow, with -t lam at column s (the identity column of
-        // row s is lam there).  Row s is scaled by lam = prod_{t<s} z_t instead
-        // (lam * v; lam^2 at column s): then every row ends up scaled by c =
-        // prod z overall, so the in-place inverse part is X = c A11^-1 itself.
-        const bool piv = pj == s;
-        zl = piv ? lam : zl;
-        const uint32_t zz = piv ? lam : z;
-        const uint32_t nn = piv ? 0u : p - t;   // p - t in (0, p]: a valid 2-product multiplier
+          for (int k = 0; k < EPL; ++k) v[k] = src_row[k];
+        }
+        constexpr bool LAZY = PDB_GJ_LAZYP && !P31 && EPL >= 4;
+        const GjPiv gp = gj_gauss_jordan<B, LPM, LAZY>(v, pj, pc, l, omask, PDB_GJ_GELAST && mrem == 0, m);
+        if (gp.lam == 0) return false;   // lam = prod z_s: zero iff a pivot vanished
+        // det(A11) = z_{B-1} / (lambda_1 ... lambda_{B-2}): row pj holds lambda_pj = zl;
+        // each row's first lane keeps its factors, the group multiplies them once per node
+        den = gj_mont(den, (pj >= 1 && pj <= B - 2 && l % LPR == 0) ? gp.zl : one, m);
+        num = gj_mont(num, gp.zlast, m);
+        if (mrem == 0) return true;
+        cR = gp.lam;   // c = prod z_s
+        // negX = -X  ->  NX[pj][pc + k]
 #pragma unroll
         for (int k = 0; k < EPL; ++k) {
-          if (!live(k)) continue;
-          uint32_t a = v[k], b = prow[k];
-          if (k == s % EPL) {   // the only element of this lane that can sit in column s
-            const bool diag = pc == s - s % EPL;
-            a = diag ? (piv ? lam : 0u) : a;
-            b = diag ? lam : b;
-          }
-          v[k] = gj_red2(mad_wide(zz, a, mad_wide(nn, b, 0ull)), m);
+          const uint32_t x = LAZY ? csub(v[k], p) : v[k];
+          NX[gj_nx_row(pj) + pc + k] = x ? p - x : 0u;
         }
-        if (s == B - 1) zlast = z;
-        lam = gj_mont(lam, z, m);
       }
-      if (lam == 0) return false;   // lam = prod z_s: zero iff a pivot vanished
-      // det(A11) = z_{B-1} / (lambda_1 ... lambda_{B-2}): row pj holds lambda_pj = zl;
-      // each row's first lane keeps its factors, the group multiplies them once per node
-      den = gj_mont(den, (pj >= 1 && pj <= B - 2 && l % LPR == 0) ? zl : one, m);
-      num = gj_mont(num, zlast, m);
-      if (mrem == 0) return true;
-      const uint32_t cR = lam;   // c = prod z_s
       Q = gj_mont(Q, cR, m);
       if (K + B < RP - TAIL4) C8 = gj_mont(C8, Q, m);   // the next block has 8 pivots
       else C4 = gj_mont(C4, Q, m);
-      // negX = -X  ->  NX[pj][pc + k]
-#pragma unroll
-      for (int k = 0; k < EPL; ++k) NX[gj_nx_row(pj) + pc + k] = v[k] ? p - v[k] : 0u;
       __syncwarp(omask);
       // ---------------- M: negM = negX * A12, in place in the pivot rows ----------------
-      // compile-time orders with 16 lanes: the idle-lane-free variants where mrem = 24
-      constexpr bool FIT = RPC > 0 && LPM == 16 && B == GJ_B;
       if (PDB_GJ_ABL == 1) {
       } else if (FIT && mrem == 24) {
         gj_mpass24<P31, B>(A, NX, S, K, l, omask, m);
@@ -908,6 +1049,10 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
 #pragma unroll
         for (int i = 0; i < 2; ++i) c4 = gj_mont(c4, c4, m);
         num_out[node] = num;
+        if (PDB_GJ_P44) {
+          const uint32_t a2 = gj_mont(aprod, aprod, m);
+          c4 = gj_mont(c4, gj_mont(a2, a2, m), m);
+        }
         den_out[node] = gj_mont(den, gj_mont(c, c4, m), m);
       } else {
         den_out[node] = 0u;
