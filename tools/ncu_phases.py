@@ -2,6 +2,8 @@
 
     python tools/ncu_phases.py report.ncu-rep obj.o FILL,P_FIRST,P_LAST,M,T [nodes]
 
+(FILL, M and T may be several lines joined by '+'.)
+
 The line numbers are det_gj.cuh lines of the kernel body (fill call, first and
 last line of the pivot-block phase, M-pass call, T-pass call); an instruction
 belongs to a phase when any frame of its inlining chain (nvdisasm -gi) is on
@@ -54,7 +56,9 @@ def chains(obj, want):
 
 def main():
     rep, obj = sys.argv[1], sys.argv[2]
-    FILL, P0, P1, MP, TP = (int(x) for x in sys.argv[3].split(","))
+    # each field may list several call lines joined by '+' (e.g. the M pass has one call per variant)
+    FILL, P0, P1, MP, TP = ({int(y) for y in x.split("+")} for x in sys.argv[3].split(","))
+    P0, P1 = min(P0), max(P1)
     nd = int(sys.argv[4]) if len(sys.argv) > 4 else 262144
     _, rows = ncu_rows(rep)
     funcs, cands = chains(obj, ["det_gj_kernel", "FusedSrc"])
@@ -68,11 +72,11 @@ def main():
     lmap = funcs[fn]
 
     def phase(lines):
-        if TP in lines:
+        if TP & set(lines):
             return "T"
-        if MP in lines:
+        if MP & set(lines):
             return "M"
-        if FILL in lines:
+        if FILL & set(lines):
             return "fill"
         if any(P0 <= x <= P1 for x in lines):
             return "P"
