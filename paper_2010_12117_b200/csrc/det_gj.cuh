@@ -658,36 +658,75 @@ __device__ __forceinline__ GjPiv gj_gauss_jordan(uint32_t (&v)[EPL], int pj, int
   return {lam, zl, zlast};
 }
 
+// ---- 4x4 adjugate, one entry per lane of a 16-lane group ------------------------------
+// M: 4x4 in shared memory (row stride S).  Lanes 0..11 form the 2x2 minors of
+// rows (0, 1) (index q) and rows (2, 3) (6 + q) for the column pairs q = (0,1),
+// (0,2), (0,3), (1,2), (1,3), (2,3); lane (i, j) then expands the cofactor of
+// entry (j, i) along the partner row j^1:
+//   adj_ij = sum_{t<3} (-1)^(i+j+t) M[j^1][k_t] * minor(other row pair, columns {0..3} \ {i, k_t}),
+// k_t the t-th column other than i (table checked against the adjugate identity
+// adj M = det(M) I on random matrices).  det(M) = sum_t M[0][t] adj[t][0].
+// Returns adj_ij (canonical); det in every lane.  mins: 12 words of scratch.
+__device__ __forceinline__ uint32_t gj_adj4(const uint32_t* M, int S, uint32_t* mins, int l, unsigned omask,
+                                           const Mod32& m, uint32_t& det) {
+  const uint32_t p = m.p;
+  const int i = l >> 2, j = l & 3;
+  if (l < 12) {
+    const int q = l < 6 ? l : l - 6;
+    const int ca = q < 3 ? 0 : (q < 5 ? 1 : 2), cb = q < 3 ? q + 1 : (q < 5 ? q - 1 : 3);
+    const uint32_t* R0 = M + (l < 6 ? 0 : 2) * S;
+    const uint32_t* R1 = R0 + S;
+    mins[l] = gj_red2(mad_wide(R0[ca], R1[cb], mad_wide(p - R1[ca], R0[cb], 0ull)), m);
+  }
+  __syncwarp(omask);
+  const uint32_t* R = M + (j ^ 1) * S;
+  const int off = j < 2 ? 6 : 0;
+  uint64_t acc = 0;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const int k = t + (t >= i);
+    const int a = i < k ? i : k, b = i < k ? k : i;
+    const int mu = off + 5 - (a + b - 1 + (a > 0));   // complement of the column pair {a, b}
+    const uint32_t e = R[k];
+    acc = mad_wide(((i + j + t) & 1) ? p - e : e, mins[mu], acc);   // p - e <= p: a valid multiplier
+  }
+  const uint32_t adj = gj_red2(acc, m);
+  uint32_t row0[4];
+  gj_ld<4>(M, row0);
+  uint64_t d = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) d = mad_wide(row0[t], __shfl_sync(omask, adj, 4 * t, 16), d);
+  det = gj_red(d, m);
+  return adj;
+}
+
 // ---- P by 4x4 blocks (8x8 pivot block, 16 lanes: one 4x4 entry per lane) --------------
-// A11 = [[A, B], [C, D]].  Gauss-Jordan on A (X_A = a A^-1), N = -X_A B,
-// S = a D + C N = a Sigma (Sigma = D - C A^-1 B), Gauss-Jordan on S
-// (X_S = s S^-1), then X = c A11^-1 with c = a s from the block inverse:
+// A11 = [[A, B], [C, D]].  X_A = adj(A) (= a A^-1, a = det A), N = -X_A B,
+// S = a D + C N = a Sigma (Sigma = D - C A^-1 B), X_S = adj(S) (= s S^-1,
+// s = det S), then X = c A11^-1 with c = a s from the block inverse:
 //   Y = a X_S = s Sigma^-1,  X22 = a Y,  X12 = N Y,  Z = X_S (C X_A),
 //   X21 = -a Z,  X11 = s X_A - N Z.
-// Two 4-step eliminations (2 products and a reduction per entry and step) plus
-// six 4x4 products with one reduction per 4-5 products: ~720 products and ~270
-// reductions per block against 1024 and 512 for the 8-step elimination.
-// det(A11) = det(A) det(S) / a^4: the a^4 is collected in aprod (den *= aprod^4
-// once per node).  Scratch: X_A and N in negX rows 0-3, then the dead pivot
-// block itself.  Returns false if a pivot vanished (A or S singular, i.e. a
-// leading principal minor of A11 is zero -- the same nodes the 8-step
-// elimination flags).
+// Two adjugates (gj_adj4: 2 + 3 + 4 products per lane, no elimination chain)
+// plus six 4x4 products with one reduction per 4-5 products, against 8
+// elimination steps of 2 products and a reduction per entry.
+// det(A11) = det(A) det(Sigma) = a s / a^4: num *= s, and the a's are
+// collected in aprod (den *= aprod^3 once per node).  Scratch: X_A and N in
+// negX rows 0-3, the minors in negX row 4, then the dead pivot block itself.
+// Returns false if A or Sigma is singular (the node goes to det_robust).
 __device__ __forceinline__ bool gj_pinv44(uint32_t* A, uint32_t* NX, int S, int K, int l, unsigned omask,
-                                          const Mod32& m, uint32_t& num, uint32_t& den, uint32_t& aprod,
-                                          uint32_t& cR) {
-  const uint32_t p = m.p, one = m.r1;
+                                          const Mod32& m, uint32_t& num, uint32_t& aprod, uint32_t& cR) {
+  const uint32_t p = m.p;
   const int i = l >> 2, j = l & 3;
   uint32_t* P0 = A + K * S + K;   // the pivot block, row stride S
   auto neg = [&](uint32_t x) { return x ? p - x : 0u; };
-  // X_A
-  uint32_t xa[1] = {P0[i * S + j]};
-  const GjPiv ga = gj_gauss_jordan<4, 16, false>(xa, i, j, l, omask, false, m);
-  if (ga.lam == 0) return false;
-  const uint32_t aR = ga.lam;
+  // X_A = adj(A), a = det(A)
+  uint32_t aR;
+  const uint32_t xa = gj_adj4(P0, S, NX + gj_nx_row(4), l, omask, m, aR);
+  if (aR == 0) return false;
   uint32_t crow[4];
   gj_ld<4>(P0 + (4 + i) * S, crow);
   const uint32_t dv = P0[(4 + i) * S + 4 + j];
-  NX[i * GJ_B + j] = xa[0];
+  NX[i * GJ_B + j] = xa;
   __syncwarp(omask);
   // N = -X_A B
   {
@@ -700,18 +739,20 @@ __device__ __forceinline__ bool gj_pinv44(uint32_t* A, uint32_t* NX, int S, int 
   }
   __syncwarp(omask);
   // S = a D + C N
-  uint32_t sv[1];
   {
     uint64_t acc = mad_wide(dv, aR, 0ull);
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc = mad_wide(crow[q], NX[q * GJ_B + 4 + j], acc);
-    sv[0] = gj_red(acc, m);
+    // every read of the pivot block is done (A, B; C and D are in registers): scratch from here
+    P0[i * S + j] = gj_red(acc, m);        // S at the A position
   }
-  const GjPiv gs = gj_gauss_jordan<4, 16, false>(sv, i, j, l, omask, false, m);
-  if (gs.lam == 0) return false;
-  const uint32_t sR = gs.lam, xs = sv[0];
+  __syncwarp(omask);
+  // X_S = adj(S), s = det(S)
+  uint32_t sR;
+  const uint32_t xs = gj_adj4(P0, S, NX + gj_nx_row(4), l, omask, m, sR);
+  if (sR == 0) return false;
   const uint32_t y = gj_mont(xs, aR, m);   // Y = a X_S
-  __syncwarp(omask);                       // every read of the pivot block is done: scratch from here
+  __syncwarp(omask);
   P0[i * S + j] = xs;                      // X_S at the A position
   P0[i * S + 4 + j] = y;                   // Y at the B position
   {
@@ -736,7 +777,7 @@ __device__ __forceinline__ bool gj_pinv44(uint32_t* A, uint32_t* NX, int S, int 
   {
     uint32_t nr[4];                        // X12 = N Y, X11 = s X_A + N (-Z)
     gj_ld<4>(NX + i * GJ_B + 4, nr);
-    uint64_t a12 = 0, a11 = mad_wide(xa[0], sR, 0ull);
+    uint64_t a12 = 0, a11 = mad_wide(xa, sR, 0ull);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       a12 = mad_wide(nr[q], P0[q * S + 4 + j], a12);
@@ -750,9 +791,8 @@ __device__ __forceinline__ bool gj_pinv44(uint32_t* A, uint32_t* NX, int S, int 
   NX[gj_nx_row(i) + 4 + j] = neg(x12);
   NX[gj_nx_row(4 + i) + j] = gj_mont(zp, aR, m);            // -X21 = a Z
   NX[gj_nx_row(4 + i) + 4 + j] = gj_mont(y, neg(aR), m);    // -X22 = -a Y
-  // det(A) det(S): lambda_1, lambda_2 of A on lanes (1, 0), (2, 0), of S on (1, 1), (2, 1)
-  den = gj_mont(den, (i >= 1 && i <= 2 && j < 2) ? (j == 0 ? ga.zl : gs.zl) : one, m);
-  num = gj_mont(num, gj_mont(ga.zlast, gs.zlast, m), m);
+  // det(A11) = det(A) det(Sigma) = a s / a^4
+  num = gj_mont(num, sR, m);
   aprod = gj_mont(aprod, aR, m);
   cR = gj_mont(aR, sR, m);
   return true;
@@ -950,7 +990,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
     // (det A picks up Q^B per block: den *= C8^8 C4^4 at the end)
     uint32_t num = one, den = one, Q = one, C8 = one, C4 = one;
     uint32_t cPrev = one;   // c of the first block of a pair
-    uint32_t aprod = one;   // 4x4-block pivot blocks: product of the a's (den *= aprod^4)
+    uint32_t aprod = one;   // 4x4-block pivot blocks: product of the a = det(A)'s (den *= aprod^3)
 
     // One block of B pivots at column K; false if a pivot vanished.
     auto block = [&](auto Bc, int K) -> bool {
@@ -965,7 +1005,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       // ---------------- P: the pivot block -> X = c A11^-1 (negated into NX), c ----------------
       uint32_t cR;
       if (PDB_GJ_P44 && FIT && !P31 && mrem > 0) {
-        if (!gj_pinv44(A, NX, S, K, l, omask, m, num, den, aprod, cR)) return false;
+        if (!gj_pinv44(A, NX, S, K, l, omask, m, num, aprod, cR)) return false;
       } else {
         uint32_t v[EPL];
         {
@@ -1050,8 +1090,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         for (int i = 0; i < 2; ++i) c4 = gj_mont(c4, c4, m);
         num_out[node] = num;
         if (PDB_GJ_P44) {
-          const uint32_t a2 = gj_mont(aprod, aprod, m);
-          c4 = gj_mont(c4, gj_mont(a2, a2, m), m);
+          c4 = gj_mont(c4, gj_mont(gj_mont(aprod, aprod, m), aprod, m), m);   // aprod^3
         }
         den_out[node] = gj_mont(den, gj_mont(c, c4, m), m);
       } else {
