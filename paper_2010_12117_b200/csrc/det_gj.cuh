@@ -700,6 +700,32 @@ __device__ __forceinline__ uint32_t gj_adj4(const uint32_t* M, int S, uint32_t* 
   return adj;
 }
 
+// det(M) of a 4x4 in shared memory from its 2x2 minors (Laplace expansion by
+// rows (0, 1) and (2, 3)): s0 c5 - s1 c4 + s2 c3 + s3 c2 - s4 c1 + s5 c0.  Every lane gets it.
+__device__ __forceinline__ uint32_t gj_det4(const uint32_t* M, int S, uint32_t* mins, int l, unsigned omask,
+                                           const Mod32& m) {
+  const uint32_t p = m.p;
+  if (l < 12) {
+    const int q = l < 6 ? l : l - 6;
+    const int ca = q < 3 ? 0 : (q < 5 ? 1 : 2), cb = q < 3 ? q + 1 : (q < 5 ? q - 1 : 3);
+    const uint32_t* R0 = M + (l < 6 ? 0 : 2) * S;
+    const uint32_t* R1 = R0 + S;
+    mins[l] = gj_red2(mad_wide(R0[ca], R1[cb], mad_wide(p - R1[ca], R0[cb], 0ull)), m);
+  }
+  __syncwarp(omask);
+  uint32_t v[12];
+  gj_ld<4>(mins, *reinterpret_cast<uint32_t(*)[4]>(v));
+  gj_ld<4>(mins + 4, *reinterpret_cast<uint32_t(*)[4]>(v + 4));
+  gj_ld<4>(mins + 8, *reinterpret_cast<uint32_t(*)[4]>(v + 8));
+  uint64_t acc = mad_wide(v[0], v[11], 0ull);
+  acc = mad_wide(p - v[1], v[10], acc);
+  acc = mad_wide(v[2], v[9], acc);
+  acc = mad_wide(v[3], v[8], acc);
+  acc = mad_wide(p - v[4], v[7], acc);
+  acc = mad_wide(v[5], v[6], acc);
+  return gj_red(acc, m);
+}
+
 // ---- P by 4x4 blocks (8x8 pivot block, 16 lanes: one 4x4 entry per lane) --------------
 // A11 = [[A, B], [C, D]].  X_A = adj(A) (= a A^-1, a = det A), N = -X_A B,
 // S = a D + C N = a Sigma (Sigma = D - C A^-1 B), X_S = adj(S) (= s S^-1,
@@ -795,6 +821,46 @@ __device__ __forceinline__ bool gj_pinv44(uint32_t* A, uint32_t* NX, int S, int 
   num = gj_mont(num, sR, m);
   aprod = gj_mont(aprod, aR, m);
   cR = gj_mont(aR, sR, m);
+  return true;
+}
+
+// Last pivot block (no trailing rows): det(A11) only, = det(A) det(S) / a^4 with
+// S = a D - C adj(A) B as in gj_pinv44 (num *= det S, aprod *= a), instead of
+// eight elimination steps.  false: A or Sigma singular (det_robust decides).
+__device__ __forceinline__ bool gj_pdet44(uint32_t* A, uint32_t* NX, int S, int K, int l, unsigned omask,
+                                          const Mod32& m, uint32_t& num, uint32_t& aprod) {
+  const uint32_t p = m.p;
+  const int i = l >> 2, j = l & 3;
+  uint32_t* P0 = A + K * S + K;
+  uint32_t aR;
+  const uint32_t xa = gj_adj4(P0, S, NX + gj_nx_row(4), l, omask, m, aR);
+  if (aR == 0) return false;
+  uint32_t crow[4];
+  gj_ld<4>(P0 + (4 + i) * S, crow);
+  const uint32_t dv = P0[(4 + i) * S + 4 + j];
+  NX[i * GJ_B + j] = xa;
+  __syncwarp(omask);
+  {
+    uint32_t xr[4];                        // N = -X_A B
+    gj_ld<4>(NX + i * GJ_B, xr);
+    uint64_t acc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc = mad_wide(xr[q], P0[q * S + 4 + j], acc);
+    const uint32_t x = gj_red(acc, m);
+    NX[i * GJ_B + 4 + j] = x ? p - x : 0u;
+  }
+  __syncwarp(omask);
+  {
+    uint64_t acc = mad_wide(dv, aR, 0ull); // S = a D + C N at the A position
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc = mad_wide(crow[q], NX[q * GJ_B + 4 + j], acc);
+    P0[i * S + j] = gj_red(acc, m);
+  }
+  __syncwarp(omask);
+  const uint32_t sR = gj_det4(P0, S, NX + gj_nx_row(4), l, omask, m);
+  if (sR == 0) return false;
+  num = gj_mont(num, sR, m);
+  aprod = gj_mont(aprod, aR, m);
   return true;
 }
 
@@ -1006,6 +1072,8 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       uint32_t cR;
       if (PDB_GJ_P44 && FIT && !P31 && mrem > 0) {
         if (!gj_pinv44(A, NX, S, K, l, omask, m, num, aprod, cR)) return false;
+      } else if (PDB_GJ_P44 && FIT && !P31) {
+        return gj_pdet44(A, NX, S, K, l, omask, m, num, aprod);
       } else {
         uint32_t v[EPL];
         {
