@@ -6,7 +6,9 @@
 //
 //   for every block of 8 pivots K..K+7 (the order r is padded to RP = 8*ceil(r/8)
 //   with an identity block, which leaves the determinant unchanged):
-//     P  division-free Gauss-Jordan on the 8x8 pivot block A11, in registers
+//     P  X = c A11^-1: in the compile-time-order kernels by 4x4 blocks and
+//        adjugates (gj_pinv44 / gj_pdet44 below: c = det(A) det(S)); otherwise
+//        division-free Gauss-Jordan on the 8x8 pivot block A11, in registers
 //        (LPM/8 lanes per row, pivot rows exchanged by shuffles):
 //        X * A11 = c * I  with  c = prod z_s: the pivot row of step s is scaled by
 //        lambda_s = z_0..z_{s-1} (the others by z_s), so every row ends up scaled
