@@ -17,6 +17,7 @@ Each function names the reference code it restates:
 * `ntt_multi`          transform.py:119-159 (vn rounds: last axis + rotation)
 * `det_batch`          determinant.py:136-169 (division-free condensation)
 * `det_grid`           determinant.py:92-133  (entry-id gather, chunked, threaded)
+* `condense_trail`     determinant.py:57-84   (one matrix: determinant + pivot trail)
 * `crt_combine`        crt.py:94-130        (mixed radix digits + Horner + signed lift)
 * `reduce_entry`       tensor.py:214-237    (reduce_mod + pad_to of one entry)
 * `run_pipeline`       pipeline.py:323-404  (per prime FFT -> DET -> IFFT, then CRT)
@@ -139,6 +140,35 @@ def det_batch(mats, p):
             swaps += cols[:, a] > cols[:, b]
     det = np.where(swaps % 2 == 1, (p - det) % p, det)
     return np.where(live, det, 0)
+
+
+def condense_trail(rows, p):
+    """(det, [(step, pivot value, pivot column, flips_sign)]) of one matrix,
+    the reference's condensation with its pivot trail (pure Python ints; the
+    trail stops at the first all-zero row, det 0)."""
+    r = len(rows)
+    work = [[int(v) % p for v in row] for row in rows]
+    records, columns = [], []
+    for i in range(r):
+        row = work[i]
+        col = next((j for j, v in enumerate(row) if v), None)
+        if col is None:
+            return 0, records
+        z = row[col]
+        flips = sum(1 for c in columns if c > col) % 2 == 1
+        records.append((i, z, col, flips))
+        columns.append(col)
+        for jj in range(i + 1, r):
+            t = work[jj][col]
+            work[jj] = [(z * a - t * b) % p for a, b in zip(work[jj], row)]
+    scale, infl = 1, 1
+    for i, (_, z, _, _) in enumerate(records):
+        scale = scale * z % p
+        infl = infl * pow(z, r - 1 - i, p) % p
+    det = scale * pow(infl, -1, p) % p
+    if sum(f for *_, f in records) % 2:
+        det = (p - det) % p
+    return det, records
 
 
 def det_grid(grids, r, p, entry_ids=None, chunk=4096, workers=1):

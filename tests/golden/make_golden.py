@@ -487,7 +487,39 @@ def format_cases():
     _write("format.json", cases)
 
 
+def condense_cases():
+    """The reference's full pivot trail (determinant.py:57-84): every record's
+    step, pivot value, column and sign flag, plus the determinant."""
+    rng = random.Random(57)
+    cases = []
+    for spec in _spec_list():
+        p = spec.p
+        for r in (1, 2, 3, 4, 5, 6, 8, 9, 12, 16):
+            for kind in ("dense", "sparse", "permuted", "singular"):
+                if kind == "dense":
+                    rows = [[rng.randrange(p) for _ in range(r)] for _ in range(r)]
+                elif kind == "sparse":
+                    rows = [[rng.randrange(p) if rng.random() < 0.35 else 0 for _ in range(r)] for _ in range(r)]
+                elif kind == "permuted":
+                    perm = list(range(r))
+                    rng.shuffle(perm)
+                    rows = [[rng.randrange(1, p) if j == perm[i] else (rng.randrange(p) if j > perm[i] else 0)
+                             for j in range(r)] for i in range(r)]
+                else:
+                    rows = [[rng.randrange(p) for _ in range(r)] for _ in range(r)]
+                    if r > 1:
+                        rows[r - 1] = list(rows[0])
+                value, records = ref.condense(ref.ModMatrix.from_rows(rows, spec))
+                cases.append({"prime": [spec.p, spec.c, spec.q, spec.omega], "rows": rows, "det": int(value),
+                              "records": [[rec.step, int(rec.value), rec.column, bool(rec.flips_sign)]
+                                          for rec in records], "note": "%s r=%d" % (kind, r)})
+    _write("condense.json", cases)
+
+
 if __name__ == "__main__":
+    if "--condense" in sys.argv:
+        condense_cases()
+        sys.exit(0)
     if "--format" in sys.argv:
         format_cases()
         sys.exit(0)

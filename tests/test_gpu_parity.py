@@ -185,6 +185,21 @@ def test_condense_pivot_trail(cuda):
         assert det_mod(ModMatrix.from_rows(rows, spec)) == naive.cofactor_det(rows, 97)
 
 
+def test_condense_matches_reference_trail(cuda):
+    """The full pivot trail -- every pivot value, column and sign flag -- and the
+    determinant equal the reference's condensation (golden condense.json: dense,
+    sparse, permuted and singular matrices, r = 1..16, seven primes incl. 97,
+    2^30 < p < 2^31 and a 31-bit prime on the wide path)."""
+    n = 0
+    for case in golden("condense.json"):
+        spec = _spec(case["prime"])
+        value, records = condense(ModMatrix.from_rows(case["rows"], spec))
+        assert value == case["det"], case["note"]
+        assert [[rec.step, rec.value, rec.column, rec.flips_sign] for rec in records] == case["records"], case["note"]
+        n += 1
+    assert n == 280
+
+
 def test_crt_matches_reference_golden(cuda):
     for case in golden("crt.json"):
         specs = [find_fourier_primes(6, 1, start=p, min_count=1)[0] for p in case["primes"]]

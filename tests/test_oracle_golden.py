@@ -29,6 +29,15 @@ def test_oracle_det_matches_reference():
         assert out.tolist() == case["expected"], case["note"]
 
 
+def test_oracle_condense_trail_matches_reference():
+    """Pivot values, columns, sign flags and the determinant of the reference's
+    condensation (golden condense.json)."""
+    for case in golden("condense.json"):
+        det, records = O.condense_trail(case["rows"], case["prime"][0])
+        assert det == case["det"], case["note"]
+        assert [list(rec) for rec in records] == case["records"], case["note"]
+
+
 def test_oracle_det_chunk_and_thread_invariance():
     case = next(c for c in golden("det.json") if c["r"] == 5)
     grids = [np.array(g, dtype=np.int64) for g in case["grids"]]
