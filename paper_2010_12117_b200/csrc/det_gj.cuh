@@ -756,50 +756,46 @@ __device__ __forceinline__ bool gj_pinv44(uint32_t* A, uint32_t* NX, int S, int 
   const uint32_t dv = P0[(4 + i) * S + 4 + j];
   NX[i * GJ_B + j] = xa;
   __syncwarp(omask);
-  // N = -X_A B
+  // N = -X_A B (negX rows 0-3, columns 4-7) and P1 = C X_A (the C position: C is in registers)
   {
     uint32_t xr[4];
     gj_ld<4>(NX + i * GJ_B, xr);
-    uint64_t acc = 0;
+    uint64_t an = 0, ap = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc = mad_wide(xr[q], P0[q * S + 4 + j], acc);
-    NX[i * GJ_B + 4 + j] = neg(gj_red(acc, m));
+    for (int q = 0; q < 4; ++q) {
+      an = mad_wide(xr[q], P0[q * S + 4 + j], an);
+      ap = mad_wide(crow[q], NX[q * GJ_B + j], ap);
+    }
+    NX[i * GJ_B + 4 + j] = neg(gj_red(an, m));
+    P0[(4 + i) * S + j] = gj_red(ap, m);   // every C row was read before the last __syncwarp
   }
   __syncwarp(omask);
-  // S = a D + C N
+  // S = a D + C N at the A position
   {
     uint64_t acc = mad_wide(dv, aR, 0ull);
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc = mad_wide(crow[q], NX[q * GJ_B + 4 + j], acc);
-    // every read of the pivot block is done (A, B; C and D are in registers): scratch from here
-    P0[i * S + j] = gj_red(acc, m);        // S at the A position
+    P0[i * S + j] = gj_red(acc, m);
   }
   __syncwarp(omask);
-  // X_S = adj(S), s = det(S)
+  // X_S = adj(S), s = det(S); X_S at the D position, Y = a X_S at the B position (both dead)
   uint32_t sR;
   const uint32_t xs = gj_adj4(P0, S, NX + gj_nx_row(4), l, omask, m, sR);
   if (sR == 0) return false;
-  const uint32_t y = gj_mont(xs, aR, m);   // Y = a X_S
-  __syncwarp(omask);
-  P0[i * S + j] = xs;                      // X_S at the A position
-  P0[i * S + 4 + j] = y;                   // Y at the B position
-  {
-    uint64_t acc = 0;                      // P1 = C X_A at the C position
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc = mad_wide(crow[q], NX[q * GJ_B + j], acc);
-    P0[(4 + i) * S + j] = gj_red(acc, m);
-  }
+  const uint32_t y = gj_mont(xs, aR, m);
+  P0[(4 + i) * S + 4 + j] = xs;
+  P0[i * S + 4 + j] = y;
   __syncwarp(omask);
   uint32_t zp;
   {
-    uint32_t xr[4];                        // Z = X_S P1, -Z at the D position
-    gj_ld<4>(P0 + i * S, xr);
+    uint32_t xr[4];                        // Z = X_S P1, -Z at the A position (S is dead)
+    gj_ld<4>(P0 + (4 + i) * S + 4, xr);
     uint64_t acc = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc = mad_wide(xr[q], P0[(4 + q) * S + j], acc);
     zp = gj_red(acc, m);
   }
-  P0[(4 + i) * S + 4 + j] = neg(zp);
+  P0[i * S + j] = neg(zp);
   __syncwarp(omask);
   uint32_t x11, x12;
   {
@@ -809,7 +805,7 @@ __device__ __forceinline__ bool gj_pinv44(uint32_t* A, uint32_t* NX, int S, int 
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       a12 = mad_wide(nr[q], P0[q * S + 4 + j], a12);
-      a11 = mad_wide(nr[q], P0[(4 + q) * S + 4 + j], a11);
+      a11 = mad_wide(nr[q], P0[q * S + j], a11);
     }
     x12 = gj_red(a12, m);
     x11 = gj_red(a11, m);
