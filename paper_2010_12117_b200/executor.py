@@ -364,9 +364,12 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
         lo, hi = shard.coefficient_range(nodes, rank, size)
         block = shard.exchange_residues(residues, whole, rank, size) if whole else None
         if slab_primes:
+            # partial rows of every slab prime, summed over the ranks straight into
+            # this rank's coefficient range (the only exchange besides the all-to-all)
             slab_rows = _slab_primes(dp, slab_primes, work, det_buf, scratch, det_chunk, rank, size, cfg, events,
-                                     torch, stream)
-            block = torch.cat([block, slab_rows[:, lo:hi]]) if whole else slab_rows[:, lo:hi]
+                                     torch, stream, partial=True)
+            slab_block = shard.reduce_scatter_rows(slab_rows, [primes[pi] for pi in slab_primes], rank, size)
+            block = torch.cat([block, slab_block]) if whole else slab_block
         del residues
         t4 = _Timer(torch, stream).mark()
         coeffs = sharded_lift(block, primes, nodes, lo, rank, size)
@@ -394,10 +397,13 @@ def execute(m: PolyMatrix, pl: Plan, cfg: PipelineConfig, ws):
     return result, timings
 
 
-def _slab_primes(dp: DevicePlan, primes, work, det_buf, scratch, chunk, rank, size, cfg, events, torch, stream):
-    """Slab-sharded primes (shard.py): every rank evaluates the entries, computes
-    the determinants of its slab of the slowest axis, all-gathers the slabs and
-    runs the inverse NTT of the full grid."""
+def _slab_primes(dp: DevicePlan, primes, work, det_buf, scratch, chunk, rank, size, cfg, events, torch, stream,
+                 partial: bool = False):
+    """Slab-sharded primes (shard.py): every rank evaluates the entries and
+    computes the determinants of its slab of the slowest axis.  partial: the
+    rank interpolates its slab alone (zero elsewhere) and returns partial
+    coefficient rows for shard.reduce_scatter_rows; otherwise the slabs are
+    all-gathered and every rank interpolates the full grid (u64 path)."""
     pl = dp.pl
     k0 = dp.klen[0]           # slabs of the kept nodes' slowest axis
     inner = dp.sel // k0
@@ -410,7 +416,12 @@ def _slab_primes(dp: DevicePlan, primes, work, det_buf, scratch, chunk, rank, si
         _fft_stage(dp, ctx, work, None, pi, cfg)
         t1 = _Timer(torch, stream).mark()
         _det_range(dp, ctx, work, det_buf, scratch, chunk, lo * inner, (hi - lo) * inner)
-        full = shard.gather_slabs(det_buf[lo * inner: hi * inner], k0, inner, rank, size)
+        if partial:
+            full = det_buf[: dp.sel]
+            full[: lo * inner].zero_()
+            full[hi * inner:].zero_()
+        else:
+            full = shard.gather_slabs(det_buf[lo * inner: hi * inner], k0, inner, rank, size)
         if dp.direct:
             t2 = _Timer(torch, stream).mark()
             native.grid_interpolate(ctx, full, torch.empty_like(full), rows[j], dp.nmap, dp.box)

@@ -9,8 +9,13 @@ gloo in the CPU tests).  Two partitions, combined:
 * slab-sharded: the remaining P mod G primes (all of them when P < G, e.g.
   a one-prime plan on 8 GPUs) are split by the slowest grid axis: rank g
   computes the determinants of the nodes with a_0 in its slab (a contiguous
-  node range), the slabs are all-gathered into the full determinant grid on
-  every rank, and every rank runs that prime's (cheap) inverse NTT.
+  node range) and interpolates that slab alone, zero elsewhere -- the
+  interpolation (inverse NTT, or the kept-node interpolation) is linear, so
+  the ranks' partial coefficient rows sum to the prime's residues.  The sum
+  is a reduce-scatter over the CRT's coefficient ranges (`reduce_scatter_rows`),
+  so nothing crosses GPUs before the final exchange (partial
+  inverse DFT + reduce).  The u64 path (p >= 2^31, where G partial sums would
+  overflow 64 bits) all-gathers the determinant slabs instead (`gather_slabs`).
 
 The CRT is sharded too (the reference does it once over every coefficient,
 crt.py:94-130): an all-to-all leaves rank g with every prime's residues of
@@ -135,6 +140,33 @@ def exchange_residues(local, prime_count: int, rank: int, size: int):
         for j, pi in enumerate(my_primes(prime_count, g, size)):
             out[pi] = recv[g, j, : hi - lo]
     return out
+
+
+def reduce_scatter_rows(partial, moduli, rank: int, size: int):
+    """Sum of every rank's partial rows [S][n] (residues in [0, p_s)), reduced
+    mod p_s, restricted to this rank's coefficient range: [S][hi - lo].  The
+    sum of G values < 2^31 is exact in int64.  NCCL: one reduce_scatter_tensor;
+    other backends (gloo in the tests): an all-reduce, then the range."""
+    import torch
+    import torch.distributed as dist
+
+    rows, n = partial.shape
+    lo, hi = coefficient_range(n, rank, size)
+    mod = torch.tensor(list(moduli), dtype=torch.int64, device=partial.device).view(-1, 1)
+    wide = partial.to(torch.int64)
+    if _backend() == "nccl":
+        width = -(-n // size)
+        send = wide.new_zeros((size, rows, width))
+        for g in range(size):
+            glo, ghi = coefficient_range(n, g, size)
+            send[g, :, : ghi - glo] = wide[:, glo:ghi]
+        recv = wide.new_empty((rows, width))
+        dist.reduce_scatter_tensor(recv.view(-1), send.view(-1))
+        out = recv[:, : hi - lo]
+    else:
+        dist.all_reduce(wide)
+        out = wide[:, lo:hi]
+    return (out % mod).to(partial.dtype)
 
 
 def gather_compact(count: int, limbs, idx, neg, width: int, rank: int, size: int):

@@ -107,6 +107,50 @@ def test_slab_sharded_primes_match_single_process(tmp_path, size):
     assert np.array_equal(got, np.stack([_residues(m, pl, pi) for pi in slab]))
 
 
+def _partial_worker(rank, size, port, case, force_rs, out_path):
+    """Slab-sharded primes without a mid-pipeline exchange: each rank
+    interpolates its slab of determinants alone (zero elsewhere; the inverse
+    transform is linear) and the partial rows are summed by a reduce-scatter
+    over the CRT's coefficient ranges."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    m = PolyMatrix.from_dict(case["input"])
+    pl = plan(m)
+    _, slab = shard.split_primes(pl.prime_count, size)
+    n0 = pl.shape[0]
+    inner = pl.node_count // n0
+    lo, hi = shard.my_slab(n0, rank, size)
+    rows = []
+    for pi in slab:
+        spec = pl.primes[pi]
+        grids = [O.ntt_multi(O.reduce_entry(t.terms(), pl.shape, spec.p), pl.shape, spec.p, spec.omega, spec.q)
+                 for t in m.unique_entries]
+        dets = np.zeros(pl.node_count, dtype=np.int64)
+        dets[lo * inner: hi * inner] = O.det_grid([g[lo * inner: hi * inner] for g in grids], m.r, spec.p,
+                                                  m.entry_ids)
+        rows.append(O.ntt_multi(dets, pl.shape, spec.p, spec.omega, spec.q, inverse=True))
+    if force_rs:
+        shard._backend = lambda: "nccl"     # exercise reduce_scatter_tensor
+    part = shard.reduce_scatter_rows(torch.tensor(np.stack(rows), dtype=torch.int32),
+                                     [pl.primes[pi].p for pi in slab], rank, size)
+    clo, chi = shard.coefficient_range(pl.node_count, rank, size)
+    single = np.stack([_residues(m, pl, pi) for pi in slab])
+    ok = part.dtype == torch.int32 and np.array_equal(part.numpy().astype(np.int64), single[:, clo:chi])
+    flag = torch.tensor([1 if ok else 0])
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        np.save(out_path, flag.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("size,force_rs", [(2, False), (3, False), (5, False), (2, True), (3, True)])
+def test_slab_partial_rows_reduce_scatter(tmp_path, size, force_rs):
+    case = next(c for c in golden("runs.json") if c["name"] == "C2")
+    out = tmp_path / "flag.npy"
+    mp.spawn(_partial_worker, args=(size, _free_port(), case, force_rs, str(out)), nprocs=size, join=True)
+    assert np.load(out).tolist() == [1]
+
+
 def test_slab_partition_covers_axis():
     for n0 in (1, 3, 16, 256):
         for G in (1, 2, 3, 8):
