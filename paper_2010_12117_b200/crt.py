@@ -194,9 +194,31 @@ def _build_ints(host, limbs, count: int, width: int, stride: int, idx_h, neg_h, 
         native.limbs_to_digits30(limbs, count, width, stride, digits, D, nd)
         nd_h = np.ascontiguousarray(nd.cpu().numpy())
         with _PIN_LOCK:   # the staging buffer is shared; the ints are built before it is reused
+            if count >= _MT_MIN and _mt_ok():
+                return host.ints_from_digits_mt(_to_host(digits), nd_h, idx_h, neg_h, int(n), int(D), _mt_threads())
             return host.ints_from_digits(_to_host(digits), nd_h, idx_h, neg_h, int(n), int(D))
     with _PIN_LOCK:
         return host.ints_from_limbs(_to_host(limbs[:count, :width]), idx_h, neg_h, int(n), int(width))
+
+
+#: results with at least this many nonzero coefficients build their ints on threads
+_MT_MIN = 1 << 16
+
+
+def _mt_ok() -> bool:
+    """The threaded builder allocates int objects with the raw allocator (freed
+    through PyObject_Free like any large object); only without allocation hooks."""
+    import os
+    import sys
+    import tracemalloc
+    return (not tracemalloc.is_tracing() and not sys.flags.dev_mode
+            and os.environ.get("PYTHONMALLOC", "") in ("", "pymalloc", "malloc")
+            and not os.environ.get("PDB_HOST_SERIAL"))
+
+
+def _mt_threads() -> int:
+    import os
+    return max(1, min(16, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 1))
 
 
 _PINNED = {}

@@ -97,3 +97,17 @@ def test_ints_from_digits_matches_limb_path():
     assert host.ints_from_digits(digits, nd, ix, neg, n, D) == want
     with pytest.raises(IndexError):
         host.ints_from_digits(digits, nd, ix[::-1].copy(), neg, n, D)
+    # the threaded builder: same tuple for any thread count, canonical small ints,
+    # objects that behave (arithmetic, hashing, text) and free cleanly
+    for threads in (1, 3, 8):
+        got = host.ints_from_digits_mt(digits, nd, ix, neg, n, D, threads)
+        assert got == want
+    assert all(got[i] is want[i] for i, v in zip(idx, vals) if v.bit_length() <= 60 and -5 <= want[i] <= 256)
+    assert {hash(x) for x in got} == {hash(x) for x in want}
+    assert [str(got[i]) for i in idx] == [str(want[i]) for i in idx]
+    assert sum(got) == sum(want) and sum(x * x for x in got) == sum(x * x for x in want)
+    del got
+    import gc
+    gc.collect()
+    with pytest.raises(IndexError):
+        host.ints_from_digits_mt(digits, nd, ix[::-1].copy(), neg, n, D, 4)
