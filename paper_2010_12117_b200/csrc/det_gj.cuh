@@ -986,8 +986,17 @@ __device__ __forceinline__ void gj_unrolled(F&& f) {
 // trailing size, and all shared-memory addressing folds into immediates.
 // PAIR: the first two pivot blocks share one trailing update (17 products per
 // reduction, p < PDB_PAIR_PMAX; compile-time orders RPC >= 32 only).
+// Order-16 kernels are latency-bound at 2 CTAs/SM (shared memory allows 4):
+// staged ones run 4 (64 registers, +9 % at r = 16, +11 % at r = 10), fused ones
+// 3 (80 registers; at 64 the DFT-8 fill spills)
+#ifndef PDB_GJ_MINB16
+#define PDB_GJ_MINB16 4
+#endif
+#ifndef PDB_GJ_MINB16F
+#define PDB_GJ_MINB16F 3
+#endif
 template <class Src, bool DFT8, int LPM, bool P31, int RPC, bool PAIR = false>
-__global__ void __launch_bounds__(256, PDB_GJ_MINB)
+__global__ void __launch_bounds__(256, RPC == 16 ? (DFT8 ? PDB_GJ_MINB16F : PDB_GJ_MINB16) : PDB_GJ_MINB)
 det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64_t nodes,
               uint32_t* __restrict__ num_out, uint32_t* __restrict__ den_out,
               unsigned long long* __restrict__ flag_count, int64_t* __restrict__ flag_nodes, GjGeom g, Mod32 m) {
