@@ -67,10 +67,11 @@ __host__ __device__ constexpr int gj_matrix_stride(int RP, int S) {
 #define PDB_UNROLL_(n) PDB_PRAGMA_(unroll n)
 #define PDB_UNROLL(n) PDB_UNROLL_(n)
 #ifndef PDB_GJ_TUNROLL
-#define PDB_GJ_TUNROLL 2   // unroll factor of the trailing-update tile loop (measured: 2 +1.4 %, 3, 4, 8 -12 %)
+#define PDB_GJ_TUNROLL 4   // unroll factor of the trailing-update tile loop (round 2 end: 4 +0.6 % over 2, 8 -0.4 %;
+                           // before the 4x4-block pivot inverses shrank the kernel, 3/4/8 fell off an i-cache cliff)
 #endif
 #ifndef PDB_GJ_MUNROLL
-#define PDB_GJ_MUNROLL 1   // unroll factor of the M-pass item loop
+#define PDB_GJ_MUNROLL 2   // unroll factor of the M-pass item loop (with TUNROLL 4: +0.3 %)
 #endif
 
 #ifndef PDB_GJ_MINB
