@@ -530,6 +530,38 @@ def test_paired_pivot_blocks_at_the_accumulator_bound(cuda, r, p, monkeypatch):
     assert det_grid(grids, r, spec).tolist() == want
 
 
+@pytest.mark.parametrize("r", [16, 24, 40])
+def test_singular_leading_blocks_take_the_robust_path(cuda, r):
+    """The compile-time-order kernels invert each 8x8 pivot block by 4x4 blocks
+    and flag a node when a 4x4 block or its Schur complement is singular, i.e.
+    when a leading principal minor of order 4k vanishes.  Matrices built with
+    exactly such a minor (row t-1 restricted to the first t columns is a
+    combination of the rows above it, t = 4, 8, 12, ...) but generically
+    nonsingular overall go to det_robust and still equal the oracle; so do
+    singular matrices and the plain random ones around them."""
+    spec = find_fourier_primes(8, 1, start=10**9, min_count=1)[0]
+    p = spec.p
+    rng = np.random.default_rng(7 + r)
+    mats = []
+    for t in range(4, r, 4):
+        for _ in range(6):
+            m = rng.integers(0, p, (r, r))
+            coef = rng.integers(0, p, t - 1)
+            m[t - 1, :t] = (coef[:, None] * m[: t - 1, :t] % p).sum(axis=0) % p
+            mats.append(m)
+    mats.append(np.zeros((r, r), dtype=np.int64))
+    sing = rng.integers(0, p, (r, r))
+    sing[-1] = (3 * sing[0] + 5 * sing[1]) % p
+    mats.append(sing)
+    mats += [rng.integers(0, p, (r, r)) for _ in range(40)]
+    mats = np.stack(mats)
+    grids = [mats[:, e // r, e % r] for e in range(r * r)]
+    want = O.det_grid(grids, r, p).tolist()
+    got = det_grid(grids, r, spec).tolist()
+    assert got == want
+    assert sum(1 for v in want if v) >= len(want) - 2   # only the two singular ones vanish
+
+
 @pytest.mark.parametrize("r", [13, 16, 21, 24, 30, 32, 36, 40])
 def test_compile_time_and_runtime_order_kernels_agree(cuda, r, monkeypatch):
     """Padded orders 16, 24, 32 and 40 run compile-time-order kernels (the staged
