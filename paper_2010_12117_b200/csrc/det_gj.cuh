@@ -1077,6 +1077,8 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       // compile-time orders with 16 lanes: the idle-lane-free variants where mrem = 24
       constexpr bool FIT = RPC > 0 && LPM == 16 && B == GJ_B;
       // ---------------- P: the pivot block -> X = c A11^-1 (negated into NX), c ----------------
+      // 4x4 blocks + adjugates where the order is a compile-time constant (the last
+      // block only needs det(A11)); 8-step division-free Gauss-Jordan otherwise
       uint32_t cR;
       if (PDB_GJ_P44 && FIT && !P31 && mrem > 0) {
         if (!gj_pinv44(A, NX, S, K, l, omask, m, num, aprod, cR)) return false;
@@ -1110,11 +1112,9 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
       else C4 = gj_mont(C4, Q, m);
       __syncwarp(omask);
       // ---------------- M: negM = negX * A12, in place in the pivot rows ----------------
-      if (PDB_GJ_ABL == 1) {
-      } else if (FIT && mrem == 24) {
-        gj_mpass24<P31, B>(A, NX, S, K, l, omask, m);
-      } else {
-        gj_mpass_any<LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
+      if (PDB_GJ_ABL != 1) {
+        if (FIT && mrem == 24) gj_mpass24<P31, B>(A, NX, S, K, l, omask, m);
+        else gj_mpass_any<LPM, P31, B>(A, NX, S, K, mrem, l, omask, m);
       }
       __syncwarp(omask);
       // ---------------- T: trailing rows ----------------
@@ -1130,11 +1130,9 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         __syncwarp(omask);
         if (FIT && mrem == 24) gj_tpass24<false, 2 * GJ_B, true>(A, S, 0, K + B, gj_mont(cPrev, cR, m), l, m);
         else gj_tpass<2, 4, LPM, false, 2 * GJ_B, true>(A, S, 0, mrem, gj_mont(cPrev, cR, m), l, m);
-      } else if (PDB_GJ_ABL == 2) {
-      } else if (FIT && mrem == 24) {
-        gj_tpass24<P31, B>(A, S, K, K + B, cR, l, m);
-      } else {
-        gj_tpass_any<LPM, P31, B>(A, S, K, mrem, cR, l, m);
+      } else if (PDB_GJ_ABL != 2) {
+        if (FIT && mrem == 24) gj_tpass24<P31, B>(A, S, K, K + B, cR, l, m);
+        else gj_tpass_any<LPM, P31, B>(A, S, K, mrem, cR, l, m);
       }
       __syncwarp(omask);
       return true;
