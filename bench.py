@@ -527,7 +527,11 @@ def run_ours(args):
         "grid_dets_per_s": grid_rate,
         "kept_u": kept,
         "e2e": {"value": e2e, "unit": "dets/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e_ms / args.steps},
+                "ms_per_step": e_ms / args.steps,
+                "scope": "per prime: the step's entry coefficients host->device, the prime's stages "
+                         "(PrimeStages.step: evaluation, determinants, interpolation), its residue grid "
+                         "device->host; whole polynomial determinants through the public run_report are "
+                         "poly_e2e"},
         "roofline": {"bound": "int", "kernel": "det_gj_kernel<FusedSrc> (eval + elimination)",
                      "achieved": achieved / 1e9, "peak": peak_delayed / 1e9, "unit": "Gupd/s",
                      "frac": achieved / peak_delayed, "traffic": traffic, "traffic_note": traffic_note,
