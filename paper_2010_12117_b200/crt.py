@@ -211,7 +211,8 @@ def _mt_ok() -> bool:
     import os
     import sys
     import tracemalloc
-    return (not tracemalloc.is_tracing() and not sys.flags.dev_mode
+    return (hasattr(native.host_module(), "ints_from_digits_mt") and not tracemalloc.is_tracing()
+            and not sys.flags.dev_mode
             and os.environ.get("PYTHONMALLOC", "") in ("", "pymalloc", "malloc")
             and not os.environ.get("PDB_HOST_SERIAL"))
 

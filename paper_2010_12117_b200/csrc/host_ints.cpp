@@ -568,7 +568,8 @@ done:
 // PyMem_RawFree (the path every large object takes).  The caller uses it only
 // when no allocation hook is active (tracemalloc, PYTHONMALLOC=debug).  Zeros
 // are the shared immortal small int 0 (3.12+), so no refcount is touched.
-#if defined(PDB_DIRECT_LONG) && !defined(Py_REF_DEBUG) && !defined(Py_TRACE_REFS)
+// (not on free-threaded builds: their object allocator, mimalloc, frees only its own blocks)
+#if defined(PDB_DIRECT_LONG) && !defined(Py_REF_DEBUG) && !defined(Py_TRACE_REFS) && !defined(Py_GIL_DISABLED)
 #define PDB_MT_LONG 1
 static PyObject* raw_long(const uint32_t* row, Py_ssize_t k, bool negative) {
   const size_t bytes = offsetof(PyLongObject, long_value.ob_digit) + (size_t)(k ? k : 1) * sizeof(digit);
