@@ -1153,20 +1153,27 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
         if (!block(std::integral_constant<int, GJ_B>{}, K)) { ok = false; break; }
     }
 #pragma unroll
-    for (int d = 1; d < LPM; d <<= 1) den = gj_mont(den, __shfl_xor_sync(omask, den, d, LPM), m);
+    // every block by 4x4 blocks (compile-time order, 8-pivot blocks only): den and C4
+    // are never touched, det = num / (C8^8 aprod^3)
+    constexpr bool ALL44 = PDB_GJ_P44 && RPC > 0 && LPM == 16 && !P31 && TAIL4 == 0;
+    if constexpr (!ALL44) {
+#pragma unroll
+      for (int d = 1; d < LPM; d <<= 1) den = gj_mont(den, __shfl_xor_sync(omask, den, d, LPM), m);
+    }
     if (l == 0) {
       if (ok) {
         uint32_t c = C8;   // C8^8 * C4^4
 #pragma unroll
         for (int i = 0; i < 3; ++i) c = gj_mont(c, c, m);
-        uint32_t c4 = C4;
+        if constexpr (TAIL4 > 0) {
+          uint32_t c4 = C4;
 #pragma unroll
-        for (int i = 0; i < 2; ++i) c4 = gj_mont(c4, c4, m);
-        num_out[node] = num;
-        if (PDB_GJ_P44) {
-          c4 = gj_mont(c4, gj_mont(gj_mont(aprod, aprod, m), aprod, m), m);   // aprod^3
+          for (int i = 0; i < 2; ++i) c4 = gj_mont(c4, c4, m);
+          c = gj_mont(c, c4, m);
         }
-        den_out[node] = gj_mont(den, gj_mont(c, c4, m), m);
+        num_out[node] = num;
+        if (PDB_GJ_P44) c = gj_mont(c, gj_mont(gj_mont(aprod, aprod, m), aprod, m), m);   // aprod^3
+        den_out[node] = ALL44 ? c : gj_mont(den, c, m);
       } else {
         den_out[node] = 0u;
         unsigned long long k = atomicAdd(flag_count, 1ull);
