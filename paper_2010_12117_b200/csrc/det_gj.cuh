@@ -527,6 +527,7 @@ __device__ __forceinline__ void gj_tpass24(uint32_t* A, int S, int K, int c0, ui
 // passes and 16 1x4 tiles (rows c0+24..c0+31 x columns c0..c0+7) in one.
 __device__ __forceinline__ void gj_tpass_panel32(uint32_t* A, int S, int K, uint32_t cR, int l, const Mod32& m) {
   const int c0 = K + GJ_B;
+#pragma unroll
   for (int w = l; w < 48; w += 16) {
     const bool top = w < 32;
     const int i0 = c0 + (top ? 2 * (w >> 3) : GJ_B + 2 * ((w - 32) >> 1));
@@ -563,6 +564,7 @@ template <int LPM>
 __device__ __forceinline__ void gj_scale_rows(uint32_t* A, int S, int K, int c0, int ncols, uint32_t cR, int l,
                                               const Mod32& m) {
   const int per_row = ncols / 4;
+#pragma unroll
   for (int w = l; w < GJ_B * per_row; w += LPM) {
     uint32_t* a = A + (K + w / per_row) * S + c0 + 4 * (w % per_row);
     uint32_t v[4];
