@@ -385,7 +385,7 @@ static int launch_gj_geom(PrimeCtx* ctx, const GjGeom& g, Src src, const int32_t
   if (ctas_per_sm < 1) ctas_per_sm = 1;
   static const char* cenv = getenv("PDB_GJ_CTAS");   // experiments: cap resident CTAs per SM
   if (cenv && *cenv && atoi(cenv) > 0 && atoi(cenv) < ctas_per_sm) ctas_per_sm = atoi(cenv);
-  const int64_t iters = DFT8 ? nodes / g.M : (nodes + g.M - 1) / g.M;
+  const int64_t iters = DFT8 ? (nodes / 8 + g.U - 1) / g.U : (nodes + g.M - 1) / g.M;
   const int64_t cap = (int64_t)ctx->sms * ctas_per_sm;
   const int grid = (int)(iters < cap ? iters : cap);
   if (grid < 1) return 0;
@@ -470,9 +470,9 @@ static int launch_gj(PrimeCtx* ctx, int r, StagedSrc src, const int32_t* ids, in
 static int launch_gj(PrimeCtx* ctx, int r, FusedSrc src, const int32_t* ids, int64_t node_lo, int64_t nodes,
                      uint32_t* out, uint32_t* den, unsigned long long* fc, int64_t* fn, cudaStream_t st) {
   const GjGeom g = gj_pick(r, gj_lanes(r), true);
-  // whole compact last-axis rows of 8 * ulast nodes, whole u-blocks per row
+  // whole compact last-axis rows of 8 * ulast nodes (u-pairs may straddle rows)
   const int64_t klast = 8 * (int64_t)src.ulast;
-  const bool dft8 = src.E <= 8 && src.NL >= 8 && src.ulast >= 1 && src.ulast % g.U == 0 &&
+  const bool dft8 = src.E <= 8 && src.NL >= 8 && src.ulast >= 1 &&
                     node_lo % klast == 0 && nodes % klast == 0;
   if (dft8) return launch_gj_mode<FusedSrc, true>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);
   return launch_gj_mode<FusedSrc, false>(ctx, r, src, ids, node_lo, nodes, out, den, fc, fn, st);

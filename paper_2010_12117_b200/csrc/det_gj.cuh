@@ -139,29 +139,51 @@ __device__ __forceinline__ int64_t gj_node_linear(int64_t it, int slot, const Gj
 
 // DFT-8 fill geometry.  The launch covers whole compact last-axis rows of
 // 8 * ulast nodes (k = v * ulast + u, node u + (NL/8) v of the full axis; ulast
-// = NL/8 without pruning); iteration `it` takes the U consecutive u of u-block
-// ublk of compact outer row orel, i.e. full outer index o.
+// = NL/8 without pruning).  Iteration `it` takes the U consecutive u-slots
+// q = it * U + uu of the flattened (row, u) index, so a pair may straddle two
+// rows and ulast needs no rounding to a multiple of U; a slot past the last
+// row (odd rows * ulast) is a dummy: clamped reads, no output.
 struct GjD8 {
-  int64_t orel, o;
-  int ublk;
+  int64_t o;   // full outer index of this thread's fill slot
+  int u;       // its u
 };
-// Once per iteration, in 32-bit arithmetic (iterations per launch < 2^32;
-// the launch's first row orow0 comes from the host).
-__device__ __forceinline__ GjD8 gj_d8(const FusedSrc& src, int U, int64_t it) {
-  const uint32_t per_o = (uint32_t)(src.ulast / U);
+// (row, u) of u-slot it * U + uu: one 32-bit divmod of it * U (iterations per
+// launch < 2^32 / U), then at most U row wraps
+__device__ __forceinline__ void gj_slot(const FusedSrc& src, int U, int64_t it, int uu, uint32_t& orel, uint32_t& u) {
+  const uint32_t q0 = (uint32_t)it * (uint32_t)U, ul = (uint32_t)src.ulast;
+  orel = q0 / ul;
+  u = q0 - orel * ul + (uint32_t)uu;
+  if (u >= ul) {   // past the row's end: one wrap unless uu >= ulast (tiny rows)
+    u -= ul;
+    ++orel;
+    if (u >= ul) {
+      orel += u / ul;
+      u %= ul;
+    }
+  }
+}
+__device__ __forceinline__ GjD8 gj_d8(const FusedSrc& src, int U, int64_t it, int uu, int64_t rows) {
+  uint32_t orel, u;
+  gj_slot(src, U, it, uu, orel, u);
   GjD8 d;
-  d.orel = (uint32_t)it / per_o;
-  d.ublk = (int)((uint32_t)it - (uint32_t)d.orel * per_o);
+  d.u = (int)u;
+  const int64_t row = (int64_t)orel < rows ? (int64_t)orel : rows - 1;
   // full outer index of the row: a table the launcher builds for pruned maps
-  d.o = src.orow_full ? __ldg(src.orow_full + d.orel) : src.orow0 + d.orel;
+  d.o = src.orow_full ? __ldg(src.orow_full + row) : src.orow0 + row;
   return d;
 }
 
-// compact index (relative to the launch) of slot v * U + uu of iteration d8
-__device__ __forceinline__ int64_t gj_node_dft8(const FusedSrc& src, const GjD8& d8, int slot, const GjGeom& g) {
-  const int v = slot / g.U, uu = slot - v * g.U;
-  return d8.orel * 8 * (int64_t)src.ulast + (int64_t)v * src.ulast + d8.ublk * g.U + uu;
+// compact index (relative to the launch) of matrix slot v * U + uu of iteration it; -1 for a dummy slot
+__device__ __forceinline__ int64_t gj_node_dft8(const FusedSrc& src, int64_t it, int slot, int U, int64_t rows) {
+  const int v = slot / U, uu = slot - v * U;
+  uint32_t orel, u;
+  gj_slot(src, U, it, uu, orel, u);
+  if ((int64_t)orel >= rows) return -1;
+  return (int64_t)orel * 8 * src.ulast + (int64_t)v * src.ulast + u;
 }
+
+__device__ __forceinline__ int src_ulast(const FusedSrc& src) { return src.ulast; }
+__device__ __forceinline__ int src_ulast(const StagedSrc&) { return 0; }
 
 // ---- fills: the RP x RP matrices of one iteration (padding = Montgomery identity) ----
 __device__ __forceinline__ void gj_fill(const StagedSrc& src, uint32_t* mats, const GjGeom& g, const int32_t* ids,
@@ -213,7 +235,6 @@ __device__ __forceinline__ void gj_fill_dft8_e(const FusedSrc& src, uint32_t* ma
   const int r = g.r, RP = g.RP, S = g.S, U = g.U, NL = src.NL, k = src.k;
   const uint32_t p = src.p;
   const int64_t o = d8.o;
-  const int ublk = d8.ublk;
   const int step8 = NL / 8;
   uint32_t w[4], ws[4];
 #pragma unroll
@@ -222,7 +243,7 @@ __device__ __forceinline__ void gj_fill_dft8_e(const FusedSrc& src, uint32_t* ma
   const int uu = threadIdx.x % U;
   uint32_t tw[8], tws[8];
   {
-    const int u = ublk * U + uu;
+    const int u = d8.u;
     int kk = 0;
 #pragma unroll
     for (int l = 0; l < 8; ++l) {
@@ -286,7 +307,6 @@ __device__ __forceinline__ void gj_fill_dft8_dense(const FusedSrc& src, uint32_t
   const int MS = MSC ? MSC : g.MS;
   const uint32_t p = src.p;
   const int64_t o = d8.o;
-  const int ublk = d8.ublk;
   const int step8 = NL / 8;
   uint32_t w[4], ws[4];
 #pragma unroll
@@ -295,7 +315,7 @@ __device__ __forceinline__ void gj_fill_dft8_dense(const FusedSrc& src, uint32_t
   const int uu = threadIdx.x % U;
   uint32_t tw[8], tws[8];
   {
-    const int u = ublk * U + uu;
+    const int u = d8.u;
     int kk = 0;
 #pragma unroll
     for (int l = 0; l < 8; ++l) {
@@ -1034,7 +1054,8 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
   uint32_t* NX = A + RP * S;          // negX [8][8]
   const uint32_t p = m.p, one = m.r1;
 
-  const int64_t iters = DFT8 ? (nodes / g.M) : (nodes + g.M - 1) / g.M;
+  const int64_t rows8 = DFT8 && src_ulast(src) > 0 ? nodes / (8 * (int64_t)src_ulast(src)) : 0;   // compact rows
+  const int64_t iters = DFT8 ? (nodes / 8 + g.U - 1) / g.U : (nodes + g.M - 1) / g.M;
   bool dense;   // identity entry ids and no padding: affine fills
   {
     bool id = g.RP == r && g.S == r;
@@ -1046,7 +1067,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
     __syncthreads();
     GjD8 d8{};
     if constexpr (DFT8) {
-      d8 = gj_d8(src, g.U, it);
+      d8 = gj_d8(src, g.U, it, threadIdx.x % g.U, rows8);
       if (PDB_GJ_ABL != 3 || it == blockIdx.x) {
         if constexpr (RPC > 0)   // launched with 256 threads, M = 256 / LPM matrices, RP = RPC
           gj_fill_dft8<256 / LPM / 8, gj_matrix_stride(RPC, gj_row_stride(RPC)), RPC * RPC>(src, mats, g, ids, d8,
@@ -1058,7 +1079,7 @@ det_gj_kernel(Src src, const int32_t* __restrict__ ids_g, int64_t node_lo, int64
     else gj_fill(src, mats, g, ids, it, node_lo, nodes, one, dense);
     __syncthreads();
     int64_t node;
-    if constexpr (DFT8) node = gj_node_dft8(src, d8, slot, g);
+    if constexpr (DFT8) node = gj_node_dft8(src, it, slot, g.U, rows8);
     else node = gj_node_linear(it, slot, g, nodes);
     if (node < 0) continue;
 

@@ -163,7 +163,7 @@ class DevicePlan:
         self.ext = [max(t.shape[a] for t in m.unique_entries) for a in range(self.vn)]
         # pruned node set (csrc/expand.cu): determinants only where the degree
         # bound needs them, the rest of the grid is extended exactly
-        self.kept_u = kept_u(self.shape, degree_bound(m), even_last=not self.staged) \
+        self.kept_u = kept_u(self.shape, degree_bound(m)) \
             if PRUNE and not self.wide else [0] * self.vn
         self.nmap = native.node_map(self.shape, self.kept_u) if self.vn else None
         self.sel = native.node_map_size(self.nmap) if self.nmap is not None else self.nodes
@@ -192,7 +192,8 @@ def kept_u(shape, degrees, even_last: bool = False) -> list:
     """Per axis, the u-count U of the kept nodes {u + (N/8) v : u < U, v < 8}
     (0 = every node): det(M) has degree <= D_a in variable a, so
     U = floor(D_a / 8) + 1 suffices.  even_last rounds the last axis's U up to
-    even (the fused kernel evaluates pairs of u per iteration).  Axes shorter
+    even (no caller needs it since the fused kernel's u-pairs may straddle
+    rows; kept for experiments).  Axes shorter
     than 16 or with 8 U >= N keep every node."""
     out = []
     for a, (n, d) in enumerate(zip(shape, degrees)):
